@@ -1,0 +1,123 @@
+/*
+ * qrita_b200.h — C ABI of the B200-native exact Top-k / Top-p truncation library
+ * (libqrita_b200.so).  Plain pointers and sizes only; no torch or C++ types.
+ *
+ * Every entry point replaces one piece of the reference operator surface
+ * (paths relative to the reference tree, arxiv/paper_2602_01518):
+ *
+ *   qrita_topk_topp          <- pkg/src/sigmatop/engine.py:82-113   run_batch (per-row loop over
+ *                               pkg/src/sigmatop/pipeline.py:199-239 truncate_topk_topp, which
+ *                               itself dispatches to truncate_topk :140-158 / truncate_topp :161-196)
+ *                               and the paper's GPU operator shape
+ *                               _topk_topp_triton_kernel(LOGITS, BUFFER, OUTPUT, ..., K, P, ..., INPLACE)
+ *                               (PAPER.md:176-188): per-row K/P, [B,V] logits, caller scratch, in-place.
+ *   qrita_workspace_bytes    <- the paper's caller-provided BUFFER[num_programs, V]
+ *   qrita_get_status         <- pkg/src/sigmatop/core.py:120-140 validate_batch (non-finite logits,
+ *                               k out of [1,V], p out of (0,1]) as raised by engine.py:76-79
+ *   qrita_strerror           <- the ValueError texts of core.py:126-139 / pipeline.py:148-149,168-169
+ *
+ * Semantics (bit-exact against pkg/src/sigmatop/oracle.py:70-89): per row, keep the first k entries of
+ * the stable descending order (value desc, index asc, -0.0 == +0.0); renormalise the fp64 softmax over
+ * those survivors with the full-row max; keep the shortest prefix whose exactly-rounded probability sum
+ * reaches p.  k == V disables top-k, p == 1 disables top-p.  Kept entries are written bit-identical to
+ * the input, removed entries become -inf, in the input dtype.
+ *
+ * All pointers are DEVICE pointers unless stated; every call is stream-ordered and never synchronises
+ * except qrita_get_status.  The library keeps no global state besides constant tables; the caller owns
+ * every buffer.  Calls on different streams must use different workspaces.
+ */
+#ifndef QRITA_B200_H
+#define QRITA_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* cudaStream_t without pulling in the CUDA headers. */
+typedef struct CUstream_st *qrita_stream_t;
+
+/* input / output dtypes */
+enum {
+  QRITA_DTYPE_F32 = 0,
+  QRITA_DTYPE_BF16 = 1
+};
+
+/* flags — the reference EngineConfig ablation switches (engine.py:26-40) plus in-place */
+enum {
+  QRITA_SEARCH_BINARY   = 1 << 0, /* 1 pivot per pass instead of 3 (pivot_search.py:136-140, 241-244) */
+  QRITA_NO_SIGMA        = 1 << 1, /* sigma_trunc_enabled=False: never gather outliers                */
+  QRITA_FORCE_FALLBACK  = 1 << 2, /* force_fallback=True: gather, but search the full row           */
+  QRITA_NO_DUP          = 1 << 3, /* duplication_handling_enabled=False: keep whole boundary cluster*/
+  QRITA_INPLACE         = 1 << 4, /* out == logits (pipeline.py:72-74)                               */
+  QRITA_WIDE_SEARCH     = 1 << 5  /* 15 pivots per pass (B200 extension; same output)               */
+};
+
+/* return codes */
+enum {
+  QRITA_OK = 0,
+  QRITA_EINVAL_ARG = 1,   /* bad shape / pointer / flag combination        */
+  QRITA_EINVAL_K = 2,     /* some row has k outside [1, V]                  */
+  QRITA_EINVAL_P = 3,     /* some row has p outside (0, 1]                  */
+  QRITA_ENONFINITE = 4,   /* some logit is NaN or +-inf                     */
+  QRITA_EWORKSPACE = 5,   /* workspace too small / misaligned              */
+  QRITA_ECUDA = 6,        /* a CUDA runtime call failed                     */
+  QRITA_ENCCL = 7         /* reserved for the vocab-sharded variant         */
+};
+
+/* Per-row accounting, field-for-field the reference RowMetrics (core.py:72-81) plus kept_count
+ * (TruncationOutput.kept_count, core.py:84-90) and which physical path ran. */
+typedef struct qrita_row_metrics {
+  int32_t trunc_hit;         /* sigma pre-filter hit (reference rule: count > k, or mass > p) */
+  int32_t outlier_count;     /* entries strictly above the sigma threshold                    */
+  double  outlier_prob_sum;  /* top-p-only rows: softmax mass of the outliers                 */
+  int32_t k_search_iters;    /* pivot passes of the top-k search                              */
+  int32_t p_search_iters;    /* pivot passes of the top-p search                              */
+  int32_t fallback_used;     /* reference semantics: not trunc_hit                            */
+  int32_t kept_count;        /* number of kept entries                                        */
+  int32_t full_row_path;     /* 1 if this build searched the full row (miss / capacity)       */
+  int32_t reserved;
+} qrita_row_metrics;
+
+/* Bytes of device workspace needed for a [B, V] call.  The workspace must be zeroed once before its
+ * first use (qrita_workspace_init); afterwards every call leaves it clean for the next one. */
+size_t qrita_workspace_bytes(int B, int V, int dtype, int flags);
+
+/* cudaMemsetAsync(ws, 0, bytes, stream). */
+int qrita_workspace_init(void *workspace, size_t ws_bytes, qrita_stream_t stream);
+
+/*
+ * Exact Top-k + Top-p truncation of a [B, V] row-major logit matrix.
+ *   logits      device [B, ld_in] f32 or bf16 (dtype); rows are the first V columns
+ *   k           device int64 [B]   (1 <= k <= V; k == V disables top-k)
+ *   p           device float64 [B] (0 < p <= 1;  p == 1 disables top-p) — fp64, as core.py:63
+ *   out         device [B, ld_out] same dtype; may equal logits iff flags & QRITA_INPLACE
+ *   kept_count  device int32 [B] or NULL
+ *   metrics     device qrita_row_metrics [B] or NULL
+ *   sample_size prefix length of the sigma statistics (sigma_trunc.py:69-82; default 4096)
+ * Invalid k / p / non-finite rows are reported through qrita_get_status; their output is undefined.
+ */
+int qrita_topk_topp(const void *logits, int64_t ld_in, int dtype, int B, int V,
+                    const int64_t *k, const double *p,
+                    void *out, int64_t ld_out,
+                    int32_t *kept_count, qrita_row_metrics *metrics,
+                    void *workspace, size_t ws_bytes, int flags, int sample_size,
+                    qrita_stream_t stream);
+
+/* Synchronises `stream`, then reports the first failing row of the last call on this workspace:
+ * returns QRITA_OK or QRITA_EINVAL_K / QRITA_EINVAL_P / QRITA_ENONFINITE, and fills *row / *col
+ * (col = first non-finite column, or -1). */
+int qrita_get_status(const void *workspace, int B, int *row, int *col, qrita_stream_t stream);
+
+const char *qrita_strerror(int code);
+
+/* Library version, MAJOR*10000 + MINOR*100 + PATCH. */
+int qrita_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* QRITA_B200_H */

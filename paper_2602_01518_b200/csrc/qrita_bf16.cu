@@ -1,0 +1,6 @@
+// bf16 instantiation of the truncation kernels (bf16 carried as raw uint16 bits).
+#include "qrita_impl.cuh"
+
+namespace qrita {
+cudaError_t launch_bf16(const Params &P, cudaStream_t st, bool vec) { return launch_all<uint16_t>(P, st, vec); }
+}  // namespace qrita

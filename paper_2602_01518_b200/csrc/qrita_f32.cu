@@ -1,0 +1,6 @@
+// fp32 instantiation of the truncation kernels.
+#include "qrita_impl.cuh"
+
+namespace qrita {
+cudaError_t launch_f32(const Params &P, cudaStream_t st, bool vec) { return launch_all<float>(P, st, vec); }
+}  // namespace qrita

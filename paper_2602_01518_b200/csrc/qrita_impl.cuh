@@ -1,0 +1,1122 @@
+// qrita_kernels.cu — B200 (sm_100a) exact Top-k / Top-p truncation and its C ABI.
+//
+// Reference path (arxiv/paper_2602_01518, pkg/src/sigmatop):
+//   engine.run_batch (engine.py:82-113) -> pipeline.truncate_topk_topp (pipeline.py:199-239)
+//     -> sigma_trunc.{row_stats, lookup_delta_*, threshold_from, gather_outliers, is_hit}
+//        (sigma_trunc.py:69-138)
+//     -> pivot_search.{quaternary,binary}_{topk,topp} (pivot_search.py:93-244)
+//     -> pipeline.finalize_mask / _apply_plan (pipeline.py:47-78)
+// Ground truth: oracle.oracle_topk_topp (oracle.py:70-89).
+//
+// B200 design (DESIGN.md has the full story):
+//   K0 qrita_prep     one CTA per row: sigma statistics over the sample prefix (bit-replica of
+//                     numpy's pairwise mean, so thresholds equal the reference's), table lookup,
+//                     threshold key, exact fixed-point nucleus thresholds for p.
+//   K1 qrita_main     persistent, dynamically scheduled over (row, chunk) work items.  Each item
+//                     streams a 16K-element chunk once from HBM with 128-bit loads, reduces the
+//                     chunk max / non-finite flag, compacts the sigma outliers in index order into a
+//                     small per-chunk HBM scratch (warp ballot/popc + block scan) and writes the -inf
+//                     background of the output.  The CTA that completes a row's last chunk runs the
+//                     row tail: quaternary key-space pivot search over the outliers staged in shared
+//                     memory (top-k), fp64 softmax over the survivors with an exact 192-bit
+//                     fixed-point normaliser and nucleus masses (top-p), duplicate trimming by index
+//                     order, and the scatter of the kept logits.  Rows that miss the pre-filter are
+//                     searched over the full row instead.  1 HBM read + 1 HBM write per element.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+#include "qrita_types.cuh"
+
+namespace qrita {
+
+// The two 200-entry quantile tables (tables.py:13-57) — numeric data, required for
+// the sigma threshold to equal the reference's.
+static __constant__ double c_topk_table[kTableSize] = {
+     2.576,  2.319,  2.178,  2.064,  1.968,  1.892,  1.819,  1.757,  1.708,  1.659,
+     1.616,  1.568,  1.526,  1.492,  1.456,  1.420,  1.382,  1.342,  1.309,  1.280,
+     1.249,  1.221,  1.193,  1.169,  1.145,  1.121,  1.095,  1.073,  1.050,  1.030,
+     1.008,  0.987,  0.966,  0.945,  0.926,  0.910,  0.891,  0.871,  0.854,  0.837,
+     0.819,  0.803,  0.784,  0.767,  0.753,  0.734,  0.719,  0.702,  0.690,  0.675,
+     0.658,  0.640,  0.625,  0.609,  0.595,  0.578,  0.564,  0.550,  0.537,  0.521,
+     0.509,  0.495,  0.481,  0.466,  0.453,  0.439,  0.424,  0.410,  0.397,  0.383,
+     0.370,  0.356,  0.343,  0.330,  0.316,  0.302,  0.289,  0.274,  0.261,  0.247,
+     0.235,  0.223,  0.209,  0.196,  0.184,  0.172,  0.159,  0.149,  0.137,  0.124,
+     0.112,  0.100,  0.086,  0.074,  0.062,  0.050,  0.035,  0.023,  0.009, -0.003,
+    -0.015, -0.027, -0.039, -0.052, -0.063, -0.074, -0.085, -0.097, -0.109, -0.122,
+    -0.134, -0.147, -0.158, -0.171, -0.184, -0.196, -0.210, -0.223, -0.235, -0.248,
+    -0.261, -0.275, -0.289, -0.302, -0.317, -0.328, -0.341, -0.353, -0.368, -0.382,
+    -0.396, -0.410, -0.426, -0.439, -0.452, -0.465, -0.480, -0.493, -0.507, -0.521,
+    -0.537, -0.551, -0.568, -0.582, -0.597, -0.614, -0.628, -0.643, -0.658, -0.673,
+    -0.691, -0.706, -0.721, -0.738, -0.754, -0.769, -0.789, -0.808, -0.824, -0.838,
+    -0.857, -0.877, -0.893, -0.912, -0.929, -0.947, -0.965, -0.983, -1.003, -1.027,
+    -1.050, -1.070, -1.092, -1.117, -1.139, -1.162, -1.189, -1.216, -1.241, -1.272,
+    -1.300, -1.330, -1.367, -1.404, -1.441, -1.485, -1.523, -1.564, -1.607, -1.658,
+    -1.710, -1.778, -1.832, -1.901, -1.978, -2.068, -2.174, -2.325, -2.577, -3.813,
+};
+static __constant__ double c_topp_table[kTableSize] = {
+     3.656,  3.650,  3.650,  3.650,  3.626,  3.626,  3.626,  3.514,  3.514,  3.503,
+     3.503,  3.434,  3.434,  3.428,  3.428,  3.387,  3.380,  3.380,  3.376,  3.373,
+     3.373,  3.356,  3.354,  3.354,  3.291,  3.249,  3.234,  3.214,  3.198,  3.198,
+     3.185,  3.177,  3.177,  3.165,  3.164,  3.161,  3.138,  3.120,  3.115,  3.113,
+     3.093,  3.066,  3.054,  3.043,  3.037,  3.023,  2.993,  2.991,  2.976,  2.970,
+     2.952,  2.946,  2.932,  2.908,  2.902,  2.895,  2.886,  2.874,  2.861,  2.844,
+     2.836,  2.810,  2.801,  2.790,  2.784,  2.779,  2.767,  2.757,  2.745,  2.733,
+     2.723,  2.716,  2.693,  2.678,  2.671,  2.656,  2.649,  2.629,  2.611,  2.595,
+     2.592,  2.585,  2.574,  2.550,  2.543,  2.534,  2.521,  2.518,  2.497,  2.485,
+     2.468,  2.450,  2.441,  2.430,  2.412,  2.402,  2.389,  2.383,  2.377,  2.364,
+     2.349,  2.338,  2.332,  2.319,  2.310,  2.301,  2.282,  2.274,  2.266,  2.250,
+     2.242,  2.236,  2.226,  2.215,  2.207,  2.196,  2.179,  2.171,  2.162,  2.147,
+     2.135,  2.121,  2.109,  2.095,  2.085,  2.073,  2.063,  2.045,  2.030,  2.016,
+     2.003,  1.992,  1.983,  1.972,  1.960,  1.949,  1.940,  1.928,  1.912,  1.897,
+     1.881,  1.869,  1.854,  1.838,  1.824,  1.807,  1.792,  1.779,  1.764,  1.751,
+     1.739,  1.726,  1.711,  1.697,  1.685,  1.668,  1.652,  1.636,  1.622,  1.603,
+     1.585,  1.568,  1.551,  1.534,  1.513,  1.499,  1.480,  1.464,  1.441,  1.422,
+     1.394,  1.373,  1.347,  1.320,  1.296,  1.270,  1.246,  1.219,  1.190,  1.163,
+     1.135,  1.104,  1.073,  1.041,  1.006,  0.969,  0.931,  0.894,  0.851,  0.806,
+     0.757,  0.702,  0.643,  0.574,  0.498,  0.405,  0.288,  0.134, -0.110, -3.813,
+};
+
+// ------------------------------------------------------------------------------------------------
+// Element access
+// ------------------------------------------------------------------------------------------------
+template <typename T> struct Elem;
+template <> struct Elem<float> {
+  static __device__ __forceinline__ uint32_t bits(float v) { return __float_as_uint(v); }
+  static __device__ __forceinline__ float neg_inf() { return __uint_as_float(0xff800000u); }
+  static __device__ __forceinline__ float from_bits(uint32_t b) { return __uint_as_float(b); }
+};
+template <> struct Elem<uint16_t> {  // bf16 carried as raw bits; upcast to fp32 is exact
+  static __device__ __forceinline__ uint32_t bits(uint16_t v) { return ((uint32_t)v) << 16; }
+  static __device__ __forceinline__ uint16_t neg_inf() { return (uint16_t)0xff80u; }
+  static __device__ __forceinline__ uint16_t from_bits(uint32_t b) { return (uint16_t)(b >> 16); }
+};
+
+// ------------------------------------------------------------------------------------------------
+// K0: per-row preparation (sigma_trunc.py:69-103; mode routing of pipeline.py:199-218)
+// ------------------------------------------------------------------------------------------------
+// One leaf of numpy's pairwise summation (n <= 128): 8 accumulators, then the remainder.
+template <typename T, bool SQUARE>
+__device__ double leaf_sum(const T *a, int n) {
+  auto val = [&](int i) -> double {
+    const double x = (double)__uint_as_float(Elem<T>::bits(a[i]));
+    return SQUARE ? __dmul_rn(x, x) : x;
+  };
+  if (n < 8) {
+    double r = 0.0;
+    for (int i = 0; i < n; ++i) r = __dadd_rn(r, val(i));
+    return r;
+  }
+  double r[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) r[j] = val(j);
+  int i = 8;
+  for (; i < n - (n % 8); i += 8) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], val(i + j));
+  }
+  double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                         __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+  for (; i < n; ++i) res = __dadd_rn(res, val(i));
+  return res;
+}
+
+// Post-order evaluation of numpy's pairwise tree over n elements:
+//   pw(a, n) = leaf(a, n)                           if n <= 128
+//            = pw(a, n2) + pw(a + n2, n - n2)       n2 = n/2 rounded down to a multiple of 8
+// Leaves are visited left to right.  Started from the additive identity, this is bit-identical to
+// ndarray.sum on a contiguous float64 vector (verified against numpy 2.3 in tests/).
+template <class LeafFn>
+__device__ double pairwise_tree(int n, LeafFn leaf) {
+  int st_off[48], st_n[48], st_state[48];
+  double st_left[48];
+  int sp = 1;
+  st_off[0] = 0; st_n[0] = n; st_state[0] = 0;
+  double ret = 0.0;
+  bool have = false;
+  for (;;) {
+    if (!have) {
+      const int t = sp - 1;
+      if (st_n[t] <= 128) {
+        ret = leaf(st_off[t], st_n[t]);
+        --sp;
+        have = true;
+      } else {
+        int n2 = st_n[t] / 2;
+        n2 -= n2 % 8;
+        st_state[t] = 1;
+        st_off[sp] = st_off[t]; st_n[sp] = n2; st_state[sp] = 0; ++sp;
+      }
+    } else {
+      if (sp == 0) return ret;
+      const int t = sp - 1;
+      if (st_state[t] == 1) {
+        st_left[t] = ret;
+        st_state[t] = 2;
+        int n2 = st_n[t] / 2;
+        n2 -= n2 % 8;
+        st_off[sp] = st_off[t] + n2; st_n[sp] = st_n[t] - n2; st_state[sp] = 0; ++sp;
+        have = false;
+      } else {
+        ret = __dadd_rn(st_left[t], ret);
+        --sp;
+      }
+    }
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) qrita_prep(Params P) {
+  __shared__ int s_off[kMaxLeaves];
+  __shared__ int s_len[kMaxLeaves];
+  __shared__ double s_sum[kMaxLeaves];
+  __shared__ double s_sq[kMaxLeaves];
+  __shared__ int s_nl;
+  __shared__ double s_res[2];
+
+  const int row = blockIdx.x;
+  const int tid = threadIdx.x;
+  const int V = P.V;
+  const int64_t k = P.k[row];
+  const double p = P.p[row];
+  const bool bad_k = !(k >= 1 && k <= (int64_t)V);
+  const bool bad_p = !(p > 0.0 && p <= 1.0);
+  int mode;
+  if (bad_k || bad_p) mode = MODE_INVALID;
+  else if (k == V && p == 1.0) mode = MODE_PASS;
+  else if (k == V) mode = MODE_TOPP;
+  else if (p == 1.0) mode = MODE_TOPK;
+  else mode = MODE_TOPKP;
+
+  const bool want_thr = (mode == MODE_TOPK || mode == MODE_TOPP || mode == MODE_TOPKP) &&
+                        !(P.flags & QRITA_NO_SIGMA);
+  double mu = 0.0, sigma = 0.0, t = 0.0;
+  uint32_t key_thr = 0xffffffffu;
+  if (want_thr) {  // uniform per block
+    const T *a = (const T *)P.logits + (size_t)row * P.ld_in;
+    const int n = min(P.sample_size, V);
+    if (tid == 0) {
+      int nl = 0;
+      pairwise_tree(n, [&](int o, int m) -> double {
+        if (nl < kMaxLeaves) { s_off[nl] = o; s_len[nl] = m; }
+        ++nl;
+        return 0.0;
+      });
+      s_nl = nl;
+    }
+    __syncthreads();
+    const int nl = s_nl;
+    if (nl <= kMaxLeaves) {
+      for (int i = tid; i < nl; i += blockDim.x) {
+        s_sum[i] = leaf_sum<T, false>(a + s_off[i], s_len[i]);
+        s_sq[i] = leaf_sum<T, true>(a + s_off[i], s_len[i]);
+      }
+      __syncthreads();
+      if (tid == 0) {
+        int c = 0;
+        s_res[0] = pairwise_tree(n, [&](int, int) -> double { return s_sum[c++]; });
+        c = 0;
+        s_res[1] = pairwise_tree(n, [&](int, int) -> double { return s_sq[c++]; });
+      }
+    } else if (tid == 0) {  // very long samples: serial replay
+      s_res[0] = pairwise_tree(n, [&](int o, int m) -> double { return leaf_sum<T, false>(a + o, m); });
+      s_res[1] = pairwise_tree(n, [&](int o, int m) -> double { return leaf_sum<T, true>(a + o, m); });
+    }
+    __syncthreads();
+    const double sum = s_res[0], sq = s_res[1];
+    // sigma_trunc.py:78-81 — mean, E[x^2] - mu^2 floored at 0, sqrt; no FMA contraction anywhere.
+    mu = __ddiv_rn(sum, (double)n);
+    const double e2 = __ddiv_rn(sq, (double)n);
+    const double var = __dsub_rn(e2, __dmul_rn(mu, mu));
+    sigma = __dsqrt_rn(var > 0.0 ? var : 0.0);
+    // table lookup (sigma_trunc.py:85-96) and safety margin (sigma_trunc.py:99-103)
+    double delta;
+    if (mode == MODE_TOPP) {
+      int idx = (int)__dmul_rn(p, (double)kTableSize);
+      delta = c_topp_table[min(idx, kTableSize - 1)];
+    } else {
+      int idx = (int)__dmul_rn(__ddiv_rn((double)k, (double)V), (double)kTableSize);
+      delta = c_topk_table[min(idx, kTableSize - 1)];
+    }
+    const double delta_adj = __dsub_rn(delta, __dmul_rn(0.2, fabs(delta)));
+    t = __dadd_rn(mu, __dmul_rn(delta_adj, sigma));
+    // outlier iff float64(z) > t  <=>  z >= f where f is the smallest float above t
+    float f = __double2float_rd(t);
+    if (!((double)f > t)) f = nextafterf(f, __uint_as_float(0x7f800000u));
+    key_thr = key_of_bits(__float_as_uint(f));
+  }
+  if (tid == 0) {
+    RowPlan pl;
+    pl.key_thr = key_thr;
+    pl.mode = mode;
+    pl.k = k;
+    pl.p = p;
+    pl.mu = mu;
+    pl.sigma = sigma;
+    pl.t = t;
+    if (mode == MODE_TOPP || mode == MODE_TOPKP) {
+      pl.t_p = fx_round_threshold(p);
+      pl.t_sp = fx_round_threshold(nextafter(p, 2.0));
+    } else {
+      pl.t_p = fx_zero();
+      pl.t_sp = fx_zero();
+    }
+    pl.has_thr = want_thr ? 1 : 0;
+    pl.pad = 0;
+    P.plans[row] = pl;
+    P.status[row] = (bad_k ? ST_BAD_K : 0) | (bad_p ? ST_BAD_P : 0);
+    P.nf_col[row] = -1;
+  }
+}
+
+// ------------------------------------------------------------------------------------------------
+// Row tail: search + masking, executed by one whole CTA
+// ------------------------------------------------------------------------------------------------
+struct TailSmem {
+  uint32_t red_u[kWarps][48];  // per-warp partials
+  uint32_t res_u[48];          // block result
+  uint32_t u[8];               // broadcast scalars
+};
+
+// Element sources: i -> (fp32 bits, index)
+struct SrcX {  // outliers staged in shared memory (index order)
+  const uint32_t *bits;
+  const uint32_t *idx;
+  int n;
+  __device__ __forceinline__ void get(int i, uint32_t &b, uint32_t &ix) const { b = bits[i]; ix = idx[i]; }
+};
+template <typename T>
+struct SrcRow {  // the full row in global memory
+  const T *row;
+  int n;
+  __device__ __forceinline__ void get(int i, uint32_t &b, uint32_t &ix) const {
+    b = Elem<T>::bits(row[i]);
+    ix = (uint32_t)i;
+  }
+};
+
+// Pivot-pass statistics.  Bucket j holds keys in (piv[j], piv[j+1]], piv[NP] = +inf; keys <= piv[0]
+// are ignored.  Per bucket: count, min key, count of the min key, exact mass.
+template <int NP, bool MASS>
+struct Buckets {
+  uint32_t cnt[NP], mn[NP], mc[NP];
+  Fx ms[MASS ? NP : 1];
+};
+
+template <int NP, bool MASS>
+__device__ __forceinline__ void bk_init(Buckets<NP, MASS> &b) {
+#pragma unroll
+  for (int j = 0; j < NP; ++j) {
+    b.cnt[j] = 0u; b.mn[j] = 0xffffffffu; b.mc[j] = 0u;
+    if (MASS) b.ms[j] = fx_zero();
+  }
+}
+
+template <int NP, bool MASS>
+__device__ __forceinline__ void bk_add(Buckets<NP, MASS> &b, const uint32_t *piv, uint32_t key, const Fx &f) {
+  int nb = 0;
+#pragma unroll
+  for (int j = 0; j < NP; ++j) nb += (key > piv[j]) ? 1 : 0;
+#pragma unroll
+  for (int j = 0; j < NP; ++j) {
+    if (nb == j + 1) {
+      b.cnt[j] += 1u;
+      if (key < b.mn[j]) { b.mn[j] = key; b.mc[j] = 1u; }
+      else if (key == b.mn[j]) { b.mc[j] += 1u; }
+      if (MASS) b.ms[j] = fx_add(b.ms[j], f);
+    }
+  }
+}
+
+// Block reduction; result in sm.res_u = [cnt(NP) | mn(NP) | mc(NP) | 12 mass pieces per bucket].
+template <int NP, bool MASS>
+__device__ void bk_reduce(const Buckets<NP, MASS> &b, TailSmem &sm) {
+  constexpr int NV = 3 * NP + (MASS ? 12 * NP : 0);
+  static_assert(NV <= 48, "reduction scratch too small");
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int j = 0; j < NP; ++j) {
+    const uint32_t c = warp_sum(b.cnt[j]);
+    const uint32_t m = warp_min(b.mn[j]);
+    const uint32_t mc = warp_sum(b.mn[j] == m ? b.mc[j] : 0u);
+    if (lane == 0) { sm.red_u[warp][j] = c; sm.red_u[warp][NP + j] = m; sm.red_u[warp][2 * NP + j] = mc; }
+    if (MASS) {
+      uint32_t q[12];
+      fx_split(b.ms[j], q);
+#pragma unroll
+      for (int i = 0; i < 12; ++i) {
+        const uint32_t s = warp_sum(q[i]);
+        if (lane == 0) sm.red_u[warp][3 * NP + 12 * j + i] = s;
+      }
+    }
+  }
+  __syncthreads();
+  if (warp == 0) {
+    const bool act = lane < kWarps;
+#pragma unroll
+    for (int j = 0; j < NP; ++j) {
+      const uint32_t c = warp_sum(act ? sm.red_u[lane][j] : 0u);
+      const uint32_t mv = act ? sm.red_u[lane][NP + j] : 0xffffffffu;
+      const uint32_t m = warp_min(mv);
+      const uint32_t mc = warp_sum((act && mv == m) ? sm.red_u[lane][2 * NP + j] : 0u);
+      if (lane == 0) { sm.res_u[j] = c; sm.res_u[NP + j] = m; sm.res_u[2 * NP + j] = mc; }
+      if (MASS) {
+#pragma unroll
+        for (int i = 0; i < 12; ++i) {
+          const uint32_t s = warp_sum(act ? sm.red_u[lane][3 * NP + 12 * j + i] : 0u);
+          if (lane == 0) sm.res_u[3 * NP + 12 * j + i] = s;
+        }
+      }
+    }
+  }
+  __syncthreads();
+}
+
+template <int NP>
+__device__ __forceinline__ void make_pivots(uint32_t l, uint32_t r, uint32_t *piv) {
+  const unsigned long long w = (unsigned long long)(r - l);
+#pragma unroll
+  for (int j = 0; j < NP; ++j) piv[j] = l + (uint32_t)((w * (unsigned long long)(j + 1)) / (NP + 1));
+}
+
+struct KRes {
+  uint32_t K;      // k-th largest key
+  uint32_t n_gt;   // keys strictly above K
+  uint32_t n_eq;   // keys equal to K
+  int iters;
+};
+
+// Top-k boundary search over order keys.  Restates _search_topk (pivot_search.py:93-126): NP pivots
+// per pass at (j+1)/(NP+1) of [l, r], stop at the first pivot with N >= k and N - n_dup < k
+// (pivot_search.py:113-116).  Keys are integers, so the range always closes in <= 16 quaternary
+// passes — there is no range_eps collapse and no midpoint fallback.  Invariant: cnt(l) >= k > cnt(r).
+template <int NP, class Src>
+__device__ KRes search_k(const Src &src, uint32_t l, uint32_t r, uint32_t cl, uint32_t cr, uint32_t k,
+                         TailSmem &sm) {
+  int iters = 0;
+  const Fx zero = fx_zero();
+  while (r - l > 1u) {
+    uint32_t piv[NP];
+    make_pivots<NP>(l, r, piv);
+    Buckets<NP, false> b;
+    bk_init(b);
+    for (int i = threadIdx.x; i < src.n; i += kThreads) {
+      uint32_t bits, ix;
+      src.get(i, bits, ix);
+      bk_add(b, piv, key_of_bits(bits), zero);
+    }
+    bk_reduce(b, sm);
+    ++iters;
+    uint32_t cnt[NP], mn[NP], mc[NP];
+    {
+      uint32_t c = 0u, m = 0xffffffffu, x = 0u;
+#pragma unroll
+      for (int j = NP - 1; j >= 0; --j) {
+        c += sm.res_u[j];
+        if (sm.res_u[j] > 0u) { m = sm.res_u[NP + j]; x = sm.res_u[2 * NP + j]; }
+        cnt[j] = c; mn[j] = m; mc[j] = x;
+      }
+    }
+    __syncthreads();  // res_u is rewritten by the next pass
+#pragma unroll
+    for (int j = 0; j < NP; ++j)
+      if (cnt[j] >= k && cnt[j] - mc[j] < k) return KRes{mn[j], cnt[j] - mc[j], mc[j], iters};
+    uint32_t nl = l, ncl = cl, nr = r, ncr = cr;
+#pragma unroll
+    for (int j = 0; j < NP; ++j)
+      if (cnt[j] >= k) { nl = piv[j]; ncl = cnt[j]; }
+#pragma unroll
+    for (int j = NP - 1; j >= 0; --j)
+      if (cnt[j] < k) { nr = piv[j]; ncr = cnt[j]; }
+    l = nl; cl = ncl; r = nr; cr = ncr;
+  }
+  return KRes{r, cr, cl - cr, iters};
+}
+
+struct PRes {
+  uint32_t K;      // boundary key of the nucleus
+  uint32_t n_gt;   // survivors strictly above K
+  uint32_t n_eq;   // survivors equal to K
+  Fx H;            // exact mass strictly above K
+  int iters;
+};
+
+// Top-p boundary search.  Restates _search_topp + _resolve_topp (pivot_search.py:159-232) with logit
+// keys as pivots and exact masses: the crossing cluster (fsum(head) < p <= fsum(head + cluster),
+// pivot_search.py:177-191) is found directly, no resolve walk.  Invariant: M(l) >= T > M(r).
+template <int NP, class Src, class InS, class PiOf, class PiKey>
+__device__ PRes search_p(const Src &src, uint32_t l, uint32_t r, uint32_t cl, uint32_t cr, Fx Ml, Fx Mr,
+                         const Fx &T, InS in_s, PiOf pi_of, PiKey pi_key, TailSmem &sm) {
+  int iters = 0;
+  while (r - l > 1u) {
+    uint32_t piv[NP];
+    make_pivots<NP>(l, r, piv);
+    Buckets<NP, true> b;
+    bk_init(b);
+    for (int i = threadIdx.x; i < src.n; i += kThreads) {
+      uint32_t bits, ix;
+      src.get(i, bits, ix);
+      const uint32_t key = key_of_bits(bits);
+      if (key > piv[0] && in_s(key, ix)) bk_add(b, piv, key, fx_from_double(pi_of(bits, i)));
+    }
+    bk_reduce(b, sm);
+    ++iters;
+    uint32_t cnt[NP], mn[NP], mc[NP];
+    Fx M[NP];
+    {
+      uint32_t c = 0u, m = 0xffffffffu, x = 0u;
+      Fx s = fx_zero();
+#pragma unroll
+      for (int j = NP - 1; j >= 0; --j) {
+        c += sm.res_u[j];
+        if (sm.res_u[j] > 0u) { m = sm.res_u[NP + j]; x = sm.res_u[2 * NP + j]; }
+        s = fx_add(s, fx_join(&sm.res_u[3 * NP + 12 * j]));
+        cnt[j] = c; mn[j] = m; mc[j] = x; M[j] = s;
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < NP; ++j) {
+      if (cnt[j] > 0u && fx_ge(M[j], T)) {
+        const Fx Hj = fx_sub(M[j], fx_mul_u32(fx_from_double(pi_key(mn[j])), mc[j]));
+        if (!fx_ge(Hj, T)) return PRes{mn[j], cnt[j] - mc[j], mc[j], Hj, iters};
+      }
+    }
+    uint32_t nl = l, ncl = cl, nr = r, ncr = cr;
+    Fx nMl = Ml, nMr = Mr;
+#pragma unroll
+    for (int j = 0; j < NP; ++j)
+      if (fx_ge(M[j], T)) { nl = piv[j]; ncl = cnt[j]; nMl = M[j]; }
+#pragma unroll
+    for (int j = NP - 1; j >= 0; --j)
+      if (!fx_ge(M[j], T)) { nr = piv[j]; ncr = cnt[j]; nMr = M[j]; }
+    l = nl; cl = ncl; r = nr; cr = ncr; Ml = nMl; Mr = nMr;
+  }
+  return PRes{r, cr, cl - cr, Mr, iters};
+}
+
+__device__ __forceinline__ int nth_set_bit(uint32_t m, uint32_t n) {  // n >= 1
+  for (uint32_t t = 1u; t < n; ++t) m &= m - 1u;
+  return __ffs((int)m) - 1;
+}
+
+// Index of the c-th (1-based) element with key K in index order, over an index-ordered source.
+// Warp-contiguous segments: ballot/popc counts per warp, a 16-entry prefix, one warp re-scans.
+// This is the duplicate-trimming rule of _apply_plan (pipeline.py:53-56): occurrences beyond n_keep,
+// counted left to right, are dropped.
+template <class Src>
+__device__ uint32_t select_nth_eq(const Src &src, uint32_t K, uint32_t c, TailSmem &sm) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int n = src.n;
+  const int seg = ((n + kWarps - 1) / kWarps + 31) & ~31;
+  const int beg = warp * seg, end = min(n, beg + seg);
+  uint32_t cnt = 0u;
+  for (int base = beg; base < end; base += 32) {
+    const int i = base + lane;
+    bool m = false;
+    if (i < end) {
+      uint32_t bits, ix;
+      src.get(i, bits, ix);
+      m = key_of_bits(bits) == K;
+    }
+    cnt += __popc(__ballot_sync(0xffffffffu, m));
+  }
+  if (lane == 0) sm.red_u[warp][0] = cnt;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t acc = 0u;
+    int w = 0;
+    for (; w < kWarps; ++w) {
+      if (acc + sm.red_u[w][0] >= c) break;
+      acc += sm.red_u[w][0];
+    }
+    sm.u[0] = (uint32_t)w;
+    sm.u[1] = c - acc;
+    sm.u[2] = kNoCut;
+  }
+  __syncthreads();
+  const int w_star = (int)sm.u[0];
+  if (warp == w_star) {
+    uint32_t need = sm.u[1];
+    for (int base = beg; base < end; base += 32) {
+      const int i = base + lane;
+      bool m = false;
+      uint32_t ix = 0u;
+      if (i < end) {
+        uint32_t bits;
+        src.get(i, bits, ix);
+        m = key_of_bits(bits) == K;
+      }
+      const uint32_t bal = __ballot_sync(0xffffffffu, m);
+      const uint32_t pc = (uint32_t)__popc(bal);
+      if (pc >= need) {
+        if (lane == nth_set_bit(bal, need)) sm.u[2] = ix;
+        break;
+      }
+      need -= pc;
+    }
+  }
+  __syncthreads();
+  const uint32_t res = sm.u[2];
+  __syncthreads();
+  return res;
+}
+
+__device__ __forceinline__ bool kept_by(uint32_t key, uint32_t idx, uint32_t K, uint32_t cut) {
+  return key > K || (key == K && idx <= cut);
+}
+
+// Exact block-wide sum of fx(v) over the elements accepted by fn(bits, idx, i, v); also counts them.
+template <class Src, class Fn>
+__device__ Fx block_mass(const Src &src, Fn fn, uint32_t &count, TailSmem &sm) {
+  Buckets<1, true> b;
+  b.cnt[0] = 0u; b.mn[0] = 0u; b.mc[0] = 0u; b.ms[0] = fx_zero();
+  for (int i = threadIdx.x; i < src.n; i += kThreads) {
+    uint32_t bits, ix;
+    src.get(i, bits, ix);
+    double v;
+    if (fn(bits, ix, i, v)) { b.ms[0] = fx_add(b.ms[0], fx_from_double(v)); b.cnt[0] += 1u; }
+  }
+  bk_reduce(b, sm);
+  count = sm.res_u[0];
+  const Fx r = fx_join(&sm.res_u[3]);
+  __syncthreads();
+  return r;
+}
+
+// Full-row output pass.  how: 0 = kept values only (background already -inf), 1 = every element,
+// 2 = -inf where not kept (in-place).
+template <typename T>
+__device__ void write_row(const T *in, T *out, int V, uint32_t K, uint32_t cut, int how) {
+  for (int i = threadIdx.x; i < V; i += kThreads) {
+    const T v = in[i];
+    const bool kp = kept_by(key_of_bits(Elem<T>::bits(v)), (uint32_t)i, K, cut);
+    if (how == 0) { if (kp) out[i] = v; }
+    else if (how == 1) { out[i] = kp ? v : Elem<T>::neg_inf(); }
+    else { if (!kp) out[i] = Elem<T>::neg_inf(); }
+  }
+}
+
+template <typename T, int NP>
+__device__ __noinline__ void row_tail(const Params &P, int row, uint8_t *dsmem, TailSmem &sm) {
+  const int tid = threadIdx.x;
+  const int V = P.V;
+  const int nch = P.nchunks;
+  const RowPlan pl = P.plans[row];
+  const T *in = (const T *)P.logits + (size_t)row * P.ld_in;
+  T *out = (T *)P.out + (size_t)row * P.ld_out;
+  const bool inplace = (P.flags & QRITA_INPLACE) != 0;
+  const bool nodup = (P.flags & QRITA_NO_DUP) != 0;
+  const bool force_fb = (P.flags & QRITA_FORCE_FALLBACK) != 0;
+
+  uint32_t *xb = (uint32_t *)dsmem;      // [kCapX] outlier bits
+  uint32_t *xi = xb + kCapX;             // [kCapX] outlier indices
+  uint32_t *sb = xi + kCapX;             // [kCapS] survivor bits
+  uint32_t *si = sb + kCapS;             // [kCapS] survivor indices
+  double *sp = (double *)(si + kCapS);   // [kCapS] survivor exp / probability
+
+  // ---- per-row totals from the chunk statistics
+  if (tid == 0) {
+    uint32_t mx = 0u, cnt = 0u, nf = 0xffffffffu, ovf = 0u;
+    for (int c = 0; c < nch; ++c) {
+      const uint4 q = __ldcg(reinterpret_cast<const uint4 *>(P.cstats + (size_t)row * nch + c));
+      mx = max(mx, q.x);
+      cnt += q.y;
+      nf = min(nf, q.z);
+      ovf |= (q.y > (uint32_t)kCapChunk) ? 1u : 0u;
+    }
+    sm.u[0] = mx; sm.u[1] = cnt; sm.u[2] = nf; sm.u[3] = ovf;
+  }
+  __syncthreads();
+  const uint32_t maxkey = sm.u[0];
+  const uint32_t n_c = sm.u[1];
+  const uint32_t nf_col = sm.u[2];
+  const bool overflow = sm.u[3] != 0u;
+  __syncthreads();
+
+  qrita_row_metrics met;
+  memset(&met, 0, sizeof(met));
+  if (nf_col != 0xffffffffu) {  // validate_batch (core.py:124-128): reported, row left undefined
+    if (tid == 0) {
+      P.status[row] |= ST_NONFINITE;
+      P.nf_col[row] = (int32_t)nf_col;
+    }
+    return;
+  }
+  const int mode = pl.mode;
+  if (mode == MODE_INVALID) return;
+  if (mode == MODE_PASS) {  // _passthrough, pipeline.py:81-85 (the stream already copied the row)
+    if (tid == 0) {
+      met.kept_count = V;
+      if (P.kept_count) P.kept_count[row] = V;
+      if (P.metrics) P.metrics[row] = met;
+    }
+    return;
+  }
+
+  const bool sigma = pl.has_thr != 0;
+  const double m = value_of_key(maxkey);
+  met.outlier_count = sigma ? (int32_t)n_c : 0;
+
+  // ---- stage the outliers in shared memory (index order) when they fit
+  const bool x_fits = sigma && !overflow && n_c <= (uint32_t)kCapX;
+  if (x_fits) {
+    uint32_t base = 0u;
+    for (int c = 0; c < nch; ++c) {
+      const uint32_t cc = __ldcg(&P.cstats[(size_t)row * nch + c].count);
+      const size_t slot = ((size_t)row * nch + c) * kCapChunk;
+      for (uint32_t j = tid; j < cc; j += kThreads) {
+        xb[base + j] = __ldcg(P.cand_bits + slot + j);
+        xi[base + j] = __ldcg(P.cand_idx + slot + j);
+      }
+      base += cc;
+    }
+    __syncthreads();
+  }
+  const SrcX X{xb, xi, (int)n_c};
+  const SrcRow<T> R{in, V};
+
+  uint32_t Kf = 0u, cutf = kNoCut, kept = (uint32_t)V;
+  bool k_used_x = false;  // the final kept set is a subset of X
+  bool full_row = false;
+
+  // ================= top-k stage: _topk_plan, pipeline.py:88-119 =================
+  uint32_t Kk = 0u, cutk = kNoCut, n_s = (uint32_t)V;  // S = {key > Kk} U {key == Kk, idx <= cutk}
+  if (mode == MODE_TOPK || mode == MODE_TOPKP) {
+    const uint32_t k = (uint32_t)pl.k;
+    const bool hit_ref = sigma && n_c > k;  // is_hit, sigma_trunc.py:127-133
+    met.trunc_hit = (hit_ref && !force_fb) ? 1 : 0;
+    met.fallback_used = met.trunc_hit ? 0 : 1;
+    k_used_x = met.trunc_hit && x_fits;
+    KRes kr;
+    if (k_used_x) {
+      kr = search_k<NP>(X, pl.key_thr ? pl.key_thr - 1u : 0u, maxkey, n_c, 0u, k, sm);
+    } else {
+      kr = search_k<NP>(R, 0u, maxkey, (uint32_t)V, 0u, k, sm);
+      full_row = true;
+    }
+    met.k_search_iters = kr.iters;
+    Kk = kr.K;
+    uint32_t ck = k - kr.n_gt;  // n_keep = n_dup - (N - k), pipeline.py:117
+    if (nodup) ck = kr.n_eq;
+    if (ck >= kr.n_eq) cutk = kNoCut;
+    else cutk = k_used_x ? select_nth_eq(X, Kk, ck, sm) : select_nth_eq(R, Kk, ck, sm);
+    n_s = kr.n_gt + ck;
+    Kf = Kk; cutf = cutk; kept = n_s;
+  }
+
+  // ================= top-p stage: pipeline.py:161-196 (p only) and :226-239 (k then p) ============
+  if (mode == MODE_TOPP || mode == MODE_TOPKP) {
+    const Fx Tp = pl.t_p, Tsp = pl.t_sp;
+    const bool topp_only = (mode == MODE_TOPP);
+    auto in_s = [&](uint32_t key, uint32_t idx) -> bool { return topp_only || kept_by(key, idx, Kk, cutk); };
+    auto e_of = [&](uint32_t bits) -> double { return exp((double)__uint_as_float(bits) - m); };
+
+    // ---- normaliser over the survivors (core.py:93-103; oracle.py:85-86): exact sum, rounded once
+    double D;
+    bool s_cached = false;
+    uint32_t ns_cached = 0u;
+    uint32_t cnt_dummy;
+    if (!topp_only && k_used_x && n_s <= (uint32_t)kCapS) {
+      // compact S into shared memory with its exp values (order is irrelevant: sums are exact)
+      if (tid == 0) sm.u[4] = 0u;
+      __syncthreads();
+      for (int i = tid; i < X.n; i += kThreads) {
+        const uint32_t b = xb[i];
+        if (kept_by(key_of_bits(b), xi[i], Kk, cutk)) {
+          const uint32_t pos = atomicAdd(&sm.u[4], 1u);
+          sb[pos] = b; si[pos] = xi[i]; sp[pos] = e_of(b);
+        }
+      }
+      __syncthreads();
+      ns_cached = sm.u[4];
+      __syncthreads();
+      const SrcX S{sb, si, (int)ns_cached};
+      const Fx Dx = block_mass(S, [&](uint32_t, uint32_t, int i, double &v) { v = sp[i]; return true; }, cnt_dummy, sm);
+      D = fx_to_double(Dx);
+      for (int i = tid; i < (int)ns_cached; i += kThreads) sp[i] = sp[i] / D;
+      __syncthreads();
+      s_cached = true;
+    } else if (!topp_only && k_used_x) {
+      const Fx Dx = block_mass(X, [&](uint32_t b, uint32_t ix, int, double &v) {
+        if (!kept_by(key_of_bits(b), ix, Kk, cutk)) return false;
+        v = e_of(b); return true; }, cnt_dummy, sm);
+      D = fx_to_double(Dx);
+    } else {
+      const Fx Dx = block_mass(R, [&](uint32_t b, uint32_t ix, int, double &v) {
+        if (!in_s(key_of_bits(b), ix)) return false;
+        v = e_of(b); return true; }, cnt_dummy, sm);
+      D = fx_to_double(Dx);
+      full_row = true;
+    }
+    auto pi_bits = [&](uint32_t bits) -> double { return e_of(bits) / D; };
+    auto pi_key = [&](uint32_t key) -> double { return pi_bits(bits_of_key(key)); };
+
+    // ---- pick the set the nucleus search runs on: 0 = cached S, 1 = X (filtered), 2 = full row
+    int set_kind;
+    uint32_t l0, cl0;
+    Fx Ml0;
+    if (topp_only) {
+      // sigma hit for top-p: outlier mass > p (is_hit, sigma_trunc.py:134-138), judged exactly
+      bool hit_ref = false;
+      Fx Mx = fx_zero();
+      if (sigma) {
+        if (x_fits) {
+          Mx = block_mass(X, [&](uint32_t b, uint32_t, int, double &v) { v = pi_bits(b); return true; }, cnt_dummy, sm);
+        } else {
+          Mx = block_mass(R, [&](uint32_t b, uint32_t, int, double &v) {
+            if (key_of_bits(b) < pl.key_thr) return false;
+            v = pi_bits(b); return true; }, cnt_dummy, sm);
+        }
+        met.outlier_prob_sum = fx_to_double(Mx);
+        hit_ref = fx_ge(Mx, Tsp);
+      }
+      met.trunc_hit = (hit_ref && !force_fb) ? 1 : 0;
+      met.fallback_used = met.trunc_hit ? 0 : 1;
+      if (met.trunc_hit && x_fits) {
+        set_kind = 1; l0 = pl.key_thr ? pl.key_thr - 1u : 0u; cl0 = n_c; Ml0 = Mx;
+      } else {
+        set_kind = 2; l0 = 0u; cl0 = (uint32_t)V;
+        Ml0 = block_mass(R, [&](uint32_t b, uint32_t, int, double &v) { v = pi_bits(b); return true; }, cnt_dummy, sm);
+        full_row = true;
+      }
+    } else if (s_cached) {
+      set_kind = 0; l0 = 0u; cl0 = ns_cached;
+      const SrcX S{sb, si, (int)ns_cached};
+      Ml0 = block_mass(S, [&](uint32_t, uint32_t, int i, double &v) { v = sp[i]; return true; }, cnt_dummy, sm);
+    } else if (k_used_x) {
+      set_kind = 1; l0 = 0u; cl0 = n_s;
+      Ml0 = block_mass(X, [&](uint32_t b, uint32_t ix, int, double &v) {
+        if (!kept_by(key_of_bits(b), ix, Kk, cutk)) return false;
+        v = pi_bits(b); return true; }, cnt_dummy, sm);
+    } else {
+      set_kind = 2; l0 = 0u; cl0 = n_s;
+      Ml0 = block_mass(R, [&](uint32_t b, uint32_t ix, int, double &v) {
+        if (!in_s(key_of_bits(b), ix)) return false;
+        v = pi_bits(b); return true; }, cnt_dummy, sm);
+    }
+
+    if (!fx_ge(Ml0, Tsp)) {
+      // p >= fsum(all survivors): keep them all (oracle.py:45-46)
+      if (topp_only) { Kf = 0u; cutf = kNoCut; kept = (uint32_t)V; }
+    } else {
+      PRes pr;
+      const Fx zero = fx_zero();
+      if (set_kind == 0) {
+        const SrcX S{sb, si, (int)ns_cached};
+        pr = search_p<NP>(S, l0, maxkey, cl0, 0u, Ml0, zero, Tp,
+                          [&](uint32_t, uint32_t) { return true; },
+                          [&](uint32_t, int i) { return sp[i]; }, pi_key, sm);
+      } else if (set_kind == 1) {
+        pr = search_p<NP>(X, l0, maxkey, cl0, 0u, Ml0, zero, Tp, in_s,
+                          [&](uint32_t b, int) { return pi_bits(b); }, pi_key, sm);
+      } else {
+        pr = search_p<NP>(R, l0, maxkey, cl0, 0u, Ml0, zero, Tp, in_s,
+                          [&](uint32_t b, int) { return pi_bits(b); }, pi_key, sm);
+      }
+      met.p_search_iters = pr.iters;
+      // smallest j with fsum(head + j * p_b) >= p (_min_dup_count, pivot_search.py:143-156), exactly
+      if (tid == 0) {
+        const double pb = pi_key(pr.K);
+        const Fx fb = fx_from_double(pb);
+        const Fx need = fx_sub(Tp, pr.H);
+        const double jd = ceil(fx_to_double(need) / pb);
+        uint32_t j = (jd < 1.0) ? 1u : (jd > (double)pr.n_eq ? pr.n_eq : (uint32_t)jd);
+        while (j > 1u && fx_ge(fx_add(pr.H, fx_mul_u32(fb, j - 1u)), Tp)) --j;
+        while (j < pr.n_eq && !fx_ge(fx_add(pr.H, fx_mul_u32(fb, j)), Tp)) ++j;
+        sm.u[5] = j;
+      }
+      __syncthreads();
+      uint32_t j = sm.u[5];
+      __syncthreads();
+      if (nodup) j = pr.n_eq;
+      Kf = pr.K;
+      kept = pr.n_gt + j;
+      if (j >= pr.n_eq) {
+        // whole cluster (within S); if it is the top-k boundary cluster the top-k cut still applies
+        cutf = (!topp_only && pr.K == Kk) ? cutk : kNoCut;
+      } else if (set_kind == 2) {
+        cutf = select_nth_eq(R, pr.K, j, sm);
+      } else {
+        cutf = select_nth_eq(X, pr.K, j, sm);  // X is index-ordered and holds every copy of K
+      }
+    }
+  }
+
+  // ================= output: finalize_mask, pipeline.py:60-78 =================
+  if (mode == MODE_TOPP) {
+    write_row<T>(in, out, V, Kf, cutf, inplace ? 2 : 1);  // the stream left top-p-only rows alone
+  } else if (inplace) {
+    write_row<T>(in, out, V, Kf, cutf, 2);
+  } else if (k_used_x) {
+    for (int i = tid; i < X.n; i += kThreads) {
+      const uint32_t b = xb[i];
+      if (kept_by(key_of_bits(b), xi[i], Kf, cutf)) out[xi[i]] = Elem<T>::from_bits(b);
+    }
+  } else {
+    write_row<T>(in, out, V, Kf, cutf, 0);
+  }
+  if (tid == 0) {
+    met.kept_count = (int32_t)kept;
+    met.full_row_path = full_row ? 1 : 0;
+    if (P.kept_count) P.kept_count[row] = (int32_t)kept;
+    if (P.metrics) P.metrics[row] = met;
+  }
+}
+
+// ------------------------------------------------------------------------------------------------
+// K1: streaming pass + row tails
+// ------------------------------------------------------------------------------------------------
+template <typename T> struct Vec;
+template <> struct Vec<float> { using type = float4; static constexpr int W = 4; };
+template <> struct Vec<uint16_t> { using type = uint4; static constexpr int W = 8; };
+
+template <typename T>
+__device__ __forceinline__ uint32_t lane_bits(const typename Vec<T>::type &v, int w);
+template <>
+__device__ __forceinline__ uint32_t lane_bits<float>(const float4 &v, int w) {
+  return __float_as_uint(w == 0 ? v.x : w == 1 ? v.y : w == 2 ? v.z : v.w);
+}
+template <>
+__device__ __forceinline__ uint32_t lane_bits<uint16_t>(const uint4 &v, int w) {
+  const uint32_t x = (w >> 1) == 0 ? v.x : (w >> 1) == 1 ? v.y : (w >> 1) == 2 ? v.z : v.w;
+  return (w & 1) ? (x & 0xffff0000u) : (x << 16);
+}
+
+template <typename T>
+__device__ __forceinline__ typename Vec<T>::type neg_inf_vec();
+template <> __device__ __forceinline__ float4 neg_inf_vec<float>() {
+  const float n = __uint_as_float(0xff800000u);
+  return make_float4(n, n, n, n);
+}
+template <> __device__ __forceinline__ uint4 neg_inf_vec<uint16_t>() {
+  return make_uint4(0xff80ff80u, 0xff80ff80u, 0xff80ff80u, 0xff80ff80u);
+}
+
+struct MainSmem {
+  TailSmem tail;
+  uint32_t wcnt[8][kWarps];   // per (vector slot, warp) outlier counts
+  uint32_t woff[8][kWarps];   // their exclusive prefix in index order
+  uint32_t wmax[kWarps];
+  uint32_t wnf[kWarps];
+  int item;
+  int last;
+};
+
+// VEC: 16-byte aligned rows whose length is a multiple of the vector width.
+template <typename T, int NP, bool VEC>
+__global__ void __launch_bounds__(kThreads, 2) qrita_main(Params P) {
+  extern __shared__ __align__(16) uint8_t dsmem[];
+  __shared__ MainSmem ms;
+  using VT = typename Vec<T>::type;
+  constexpr int W = Vec<T>::W;
+  constexpr int U = kChunk / (kThreads * W);  // vectors per thread per chunk: 8 (f32) / 4 (bf16)
+  static_assert(U * kThreads * W == kChunk && U <= 8, "chunk shape");
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nch = P.nchunks;
+  const bool inplace = (P.flags & QRITA_INPLACE) != 0;
+
+  for (;;) {
+    if (tid == 0) ms.item = (int)atomicAdd(P.work_ctr, 1u);
+    __syncthreads();
+    const int item = ms.item;
+    if (item >= P.total_items) break;
+    const int row = item / nch, c = item - row * nch;
+    const RowPlan *plp = P.plans + row;
+    const int mode = plp->mode;
+    const uint32_t key_thr = plp->key_thr;
+    const bool gather = plp->has_thr != 0;
+    // the stream writes the -inf background of top-k rows and copies passthrough rows; top-p-only
+    // rows are written once, by their tail
+    const bool write_bg = !inplace && (mode == MODE_TOPK || mode == MODE_TOPKP || mode == MODE_INVALID);
+    const bool write_copy = !inplace && mode == MODE_PASS;
+    const bool keep_l2 = (mode == MODE_TOPP) || inplace;  // the tail re-reads these rows
+    const int c0 = c * kChunk;
+    const int n = min(kChunk, P.V - c0);
+    const T *src = (const T *)P.logits + (size_t)row * P.ld_in + c0;
+    T *dst = (T *)P.out + (size_t)row * P.ld_out + c0;
+
+    uint32_t mx = 0u, nf = 0xffffffffu;
+    uint32_t myc[U];
+    VT v[U];
+    if (VEC) {
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int e = (u * kThreads + tid) * W;
+        if (e < n) v[u] = keep_l2 ? __ldg(reinterpret_cast<const VT *>(src + e))
+                                  : __ldcs(reinterpret_cast<const VT *>(src + e));
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int e = (u * kThreads + tid) * W;
+        uint32_t cnt = 0u;
+        if (e < n) {
+#pragma unroll
+          for (int w = 0; w < W; ++w) {
+            const uint32_t b = lane_bits<T>(v[u], w);
+            const uint32_t key = key_of_bits(b);
+            mx = max(mx, key);
+            if (bits_nonfinite(b)) nf = min(nf, (uint32_t)(c0 + e + w));
+            cnt += (gather && key >= key_thr) ? 1u : 0u;
+          }
+          if (write_bg) __stcs(reinterpret_cast<VT *>(dst + e), neg_inf_vec<T>());
+          else if (write_copy) __stcs(reinterpret_cast<VT *>(dst + e), v[u]);
+        }
+        myc[u] = cnt;
+      }
+    } else {
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        uint32_t cnt = 0u;
+#pragma unroll
+        for (int w = 0; w < W; ++w) {
+          const int e = (u * kThreads + tid) * W + w;
+          if (e < n) {
+            const T x = src[e];
+            const uint32_t b = Elem<T>::bits(x);
+            const uint32_t key = key_of_bits(b);
+            mx = max(mx, key);
+            if (bits_nonfinite(b)) nf = min(nf, (uint32_t)(c0 + e));
+            cnt += (gather && key >= key_thr) ? 1u : 0u;
+            if (write_bg) dst[e] = Elem<T>::neg_inf();
+            else if (write_copy) dst[e] = x;
+          }
+        }
+        myc[u] = cnt;
+      }
+    }
+    // ---- chunk reductions: max key, first non-finite column, outlier counts per (slot, warp)
+    mx = warp_max(mx);
+    nf = warp_min(nf);
+    if (lane == 0) { ms.wmax[warp] = mx; ms.wnf[warp] = nf; }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint32_t wc = warp_sum(myc[u]);
+      if (lane == 0) ms.wcnt[u][warp] = wc;
+    }
+    __syncthreads();
+    if (warp == 0) {
+      // exclusive scan over (slot, warp) in slot-major order == index order within the chunk
+      constexpr int NE = U * kWarps;
+      constexpr int PER = (NE + 31) / 32;
+      uint32_t vals[PER];
+      uint32_t s = 0u;
+#pragma unroll
+      for (int q = 0; q < PER; ++q) {
+        const int e = lane * PER + q;
+        vals[q] = e < NE ? ms.wcnt[e / kWarps][e % kWarps] : 0u;
+        s += vals[q];
+      }
+      uint32_t incl = s;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
+      }
+      uint32_t run = incl - s;
+#pragma unroll
+      for (int q = 0; q < PER; ++q) {
+        const int e = lane * PER + q;
+        if (e < NE) ms.woff[e / kWarps][e % kWarps] = run;
+        run += vals[q];
+      }
+      const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+      const uint32_t cmax = warp_max(lane < kWarps ? ms.wmax[lane] : 0u);
+      const uint32_t cnf = warp_min(lane < kWarps ? ms.wnf[lane] : 0xffffffffu);
+      if (lane == 0) {
+        ChunkStat cs;
+        cs.maxkey = cmax; cs.count = total; cs.nf_col = cnf; cs.pad = 0u;
+        P.cstats[(size_t)row * nch + c] = cs;
+      }
+    }
+    __syncthreads();
+    // ---- outliers -> per-chunk HBM scratch, index order (order-stable compaction, gather_outliers)
+    if (gather) {
+      const size_t slot = ((size_t)row * nch + c) * kCapChunk;
+      const uint32_t lt = (1u << lane) - 1u;
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int ebase = (u * kThreads + tid) * W;
+        uint32_t pos = ms.woff[u][warp];
+#pragma unroll
+        for (int w = 0; w < W; ++w) {
+          uint32_t b = 0u;
+          if (VEC) b = lane_bits<T>(v[u], w);
+          else if (ebase + w < n) b = Elem<T>::bits(src[ebase + w]);
+          const bool cand = (ebase + w < n) && key_of_bits(b) >= key_thr;
+          const uint32_t bal = __ballot_sync(0xffffffffu, cand);
+          // elements before mine in this slot: lanes below me (all w) + my earlier w
+          if (cand) {
+            uint32_t q = pos + (uint32_t)__popc(bal & lt);
+            if (q < (uint32_t)kCapChunk) {
+              P.cand_bits[slot + q] = b;
+              P.cand_idx[slot + q] = (uint32_t)(c0 + ebase + w);
+            }
+          }
+          pos += (uint32_t)__popc(bal);
+        }
+      }
+    }
+    // ---- completion: whoever finishes a row's last chunk runs the row tail
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) {
+      const uint32_t t = atomicAdd(P.row_done + row, 1u);
+      ms.last = (t == (uint32_t)(nch - 1)) ? 1 : 0;
+    }
+    __syncthreads();
+    if (ms.last) {
+      __threadfence();
+      row_tail<T, NP>(P, row, dsmem, ms.tail);
+      __syncthreads();
+      if (tid == 0) P.row_done[row] = 0u;  // leave the workspace clean for the next call
+    }
+    __syncthreads();
+  }
+  // self-cleaning work counter
+  if (tid == 0) {
+    __threadfence();
+    const uint32_t t = atomicAdd(P.exit_ctr, 1u);
+    if (t == gridDim.x - 1) {
+      *P.work_ctr = 0u;
+      *P.exit_ctr = 0u;
+      __threadfence();
+    }
+  }
+}
+
+constexpr size_t kDynSmem = (size_t)kCapX * 8 + (size_t)kCapS * 16;
+
+template <typename T, int NP, bool VEC>
+static cudaError_t launch_main(const Params &P, cudaStream_t st) {
+  auto kern = qrita_main<T, NP, VEC>;
+  static int grid_blocks = 0;  // per instantiation
+  if (grid_blocks == 0) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDynSmem);
+    if (e != cudaSuccess) return e;
+    int dev = 0, sms = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, kDynSmem);
+    if (e != cudaSuccess) return e;
+    grid_blocks = sms * (per_sm < 1 ? 1 : per_sm);
+  }
+  int grid = grid_blocks < P.total_items ? grid_blocks : P.total_items;
+  if (grid < 1) grid = 1;
+  kern<<<grid, kThreads, kDynSmem, st>>>(P);
+  return cudaGetLastError();
+}
+
+template <typename T>
+static cudaError_t launch_all(const Params &P, cudaStream_t st, bool vec) {
+  qrita_prep<T><<<P.B, 256, 0, st>>>(P);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  if (P.flags & QRITA_SEARCH_BINARY)
+    return vec ? launch_main<T, 1, true>(P, st) : launch_main<T, 1, false>(P, st);
+  return vec ? launch_main<T, 3, true>(P, st) : launch_main<T, 3, false>(P, st);
+}
+
+}  // namespace qrita

@@ -1,0 +1,101 @@
+// qrita_types.cuh — constants, workspace records and launch parameters shared by the kernels
+// and the C ABI.
+#pragma once
+#include <cuda_runtime.h>
+#include <stddef.h>
+#include <stdint.h>
+
+#include "qrita_device.cuh"
+#include "qrita_b200.h"
+
+namespace qrita {
+
+
+// ------------------------------------------------------------------------------------------------
+// Constants
+// ------------------------------------------------------------------------------------------------
+constexpr int kTableSize = 200;  // tables.py:11
+constexpr int kChunk = 16384;    // elements per streaming work item
+constexpr int kCapChunk = 2048;  // outlier slots per chunk in the HBM scratch
+constexpr int kCapX = 8192;      // outliers staged in shared memory for the row tail
+constexpr int kCapS = 2048;      // top-k survivors whose probabilities are cached in shared memory
+constexpr int kMaxLeaves = 1024; // pairwise-sum leaves handled in parallel by qrita_prep
+
+enum Mode : int32_t { MODE_INVALID = -1, MODE_PASS = 0, MODE_TOPK = 1, MODE_TOPP = 2, MODE_TOPKP = 3 };
+enum Status : int32_t { ST_BAD_K = 1, ST_BAD_P = 2, ST_NONFINITE = 4 };
+
+// ------------------------------------------------------------------------------------------------
+// Workspace records
+// ------------------------------------------------------------------------------------------------
+struct RowPlan {
+  uint32_t key_thr;   // outlier iff key >= key_thr
+  int32_t mode;
+  int64_t k;
+  double p;
+  double mu, sigma, t;
+  Fx t_p;             // smallest exact mass whose fsum is >= p
+  Fx t_sp;            // smallest exact mass whose fsum is >= succ(p), i.e. > p
+  int32_t has_thr;    // 0: no outliers gathered for this row
+  int32_t pad;
+};
+
+struct ChunkStat {
+  uint32_t maxkey;
+  uint32_t count;     // outliers in the chunk (only the first kCapChunk are stored)
+  uint32_t nf_col;    // first non-finite column, or 0xffffffff
+  uint32_t pad;
+};
+
+struct Params {
+  const void *logits;
+  int64_t ld_in;
+  void *out;
+  int64_t ld_out;
+  int B, V, dtype, flags, sample_size;
+  const int64_t *k;
+  const double *p;
+  int32_t *kept_count;
+  qrita_row_metrics *metrics;
+  // workspace
+  RowPlan *plans;
+  ChunkStat *cstats;
+  uint32_t *cand_bits;
+  uint32_t *cand_idx;
+  uint32_t *row_done;
+  uint32_t *work_ctr;
+  uint32_t *exit_ctr;
+  int32_t *status;
+  int32_t *nf_col;
+  int nchunks;
+  int total_items;
+};
+
+// Layout: [counters | status[B] | nf_col[B] | plans[B] | row_done[B] | chunk stats | outlier slots].
+// The status block only depends on B, so qrita_get_status needs no V.
+struct WsLayout {
+  size_t ctrs, status, nf_col, plans, row_done, cstats, cand_bits, cand_idx, total;
+};
+
+inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+inline WsLayout ws_layout(int B, int V) {
+  WsLayout L;
+  const size_t nchunks = (size_t)((V + kChunk - 1) / kChunk);
+  size_t off = 0;
+  L.ctrs = off;      off = align_up(off + 64, 256);
+  L.status = off;    off = align_up(off + 4ull * (size_t)B, 256);
+  L.nf_col = off;    off = align_up(off + 4ull * (size_t)B, 256);
+  L.plans = off;     off = align_up(off + sizeof(RowPlan) * (size_t)B, 256);
+  L.row_done = off;  off = align_up(off + 4ull * (size_t)B, 256);
+  L.cstats = off;    off = align_up(off + sizeof(ChunkStat) * (size_t)B * nchunks, 256);
+  L.cand_bits = off; off = align_up(off + 4ull * (size_t)B * nchunks * kCapChunk, 256);
+  L.cand_idx = off;  off = align_up(off + 4ull * (size_t)B * nchunks * kCapChunk, 256);
+  L.total = off;
+  return L;
+}
+
+
+cudaError_t launch_f32(const Params &P, cudaStream_t st, bool vec);
+cudaError_t launch_bf16(const Params &P, cudaStream_t st, bool vec);
+
+}  // namespace qrita

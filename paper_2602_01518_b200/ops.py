@@ -1,0 +1,202 @@
+"""Device-level operator: exact Top-k / Top-p truncation of CUDA logit tensors.
+
+This is the stream-ordered call that every public entry point (engine.run_batch, the per-row
+pipeline functions, the vocab-sharded variant, bench.py) goes through.  It hands raw device pointers
+to `qrita_topk_topp` in libqrita_b200.so (include/qrita_b200.h).  PyTorch is used only for device
+memory and the current stream.  There is no CPU path: CPU tensors are rejected.
+"""
+from __future__ import annotations
+
+import ctypes
+import threading
+from dataclasses import dataclass
+from typing import Optional, Tuple, Union
+
+import torch
+
+from . import _native as N
+
+DEFAULT_SAMPLE_SIZE = 4096  # sigma_trunc.py:21
+
+_DTYPES = {torch.float32: N.DTYPE_F32, torch.bfloat16: N.DTYPE_BF16}
+
+
+@dataclass
+class TruncFlags:
+    """The reference's EngineConfig ablation switches (engine.py:26-40) as kernel flags."""
+
+    search: str = "quaternary"          # or "binary"
+    use_sigma_trunc: bool = True
+    force_fallback: bool = False
+    dup_handling: bool = True
+
+    def bits(self) -> int:
+        if self.search not in ("quaternary", "binary"):
+            raise ValueError("search_kind must be 'quaternary' or 'binary'")
+        f = 0
+        if self.search == "binary":
+            f |= N.SEARCH_BINARY
+        if not self.use_sigma_trunc:
+            f |= N.NO_SIGMA
+        if self.force_fallback:
+            f |= N.FORCE_FALLBACK
+        if not self.dup_handling:
+            f |= N.NO_DUP
+        return f
+
+
+class Workspace:
+    """Device scratch for one stream: grown on demand, zeroed once; every call leaves it clean."""
+
+    def __init__(self, device: torch.device):
+        self.device = device
+        self.buf: Optional[torch.Tensor] = None
+
+    def get(self, nbytes: int, stream: torch.cuda.Stream) -> Tuple[int, int]:
+        if self.buf is None or self.buf.numel() < nbytes:
+            self.buf = None
+            self.buf = torch.zeros(max(nbytes, 1 << 20) + 256, dtype=torch.uint8, device=self.device)
+        ptr = self.buf.data_ptr()
+        aligned = (ptr + 255) & ~255
+        return aligned, self.buf.numel() - (aligned - ptr)
+
+    def reset(self):
+        if self.buf is not None:
+            self.buf.zero_()
+
+
+_ws_lock = threading.Lock()
+_workspaces = {}
+
+
+def workspace_for(device: torch.device, stream: torch.cuda.Stream) -> Workspace:
+    key = (device.index, stream.cuda_stream)
+    with _ws_lock:
+        ws = _workspaces.get(key)
+        if ws is None:
+            ws = Workspace(device)
+            _workspaces[key] = ws
+        return ws
+
+
+def _per_row(x, b: int, dtype: torch.dtype, device: torch.device, name: str) -> torch.Tensor:
+    if isinstance(x, torch.Tensor):
+        t = x.to(device=device, dtype=dtype)
+        if t.dim() == 0:
+            t = t.expand(b)
+        if t.shape != (b,):
+            raise ValueError(f"{name} must have shape ({b},), got {tuple(t.shape)}")
+        return t.contiguous()
+    return torch.full((b,), x, dtype=dtype, device=device)
+
+
+class TruncationError(ValueError):
+    """Raised with the reference's ValueError wording (core.py:126-139)."""
+
+
+def check_status(ws_ptr: int, b: int, logits: Optional[torch.Tensor], k, p,
+                 stream: torch.cuda.Stream) -> None:
+    """Synchronise and translate the device status block into the reference's ValueError."""
+    lib = N.load()
+    row, col = ctypes.c_int(-1), ctypes.c_int(-1)
+    code = lib.qrita_get_status(ctypes.c_void_p(ws_ptr), b, ctypes.byref(row), ctypes.byref(col),
+                                ctypes.c_void_p(stream.cuda_stream))
+    if code == N.OK:
+        return
+    if code in (N.ENONFINITE, N.EINVAL_K, N.EINVAL_P):
+        raise TruncationError("invalid batch: " + "; ".join(
+            describe_invalid(logits, k, p)[:5] or [N.strerror(code)]))
+    raise RuntimeError(f"qrita_get_status failed: {N.strerror(code)}")
+
+
+def describe_invalid(logits: Optional[torch.Tensor], k, p) -> list:
+    """validate_batch's report lines (core.py:120-140), computed on the device tensors."""
+    report = []
+    if logits is not None:
+        bad = ~torch.isfinite(logits)
+        if bool(bad.any()):
+            for r, c in torch.nonzero(bad)[:5].tolist():
+                kind = "NaN" if bool(torch.isnan(logits[r, c])) else "non-finite"
+                report.append(f"{kind} logit at row {r}, col {c}")
+    v = logits.shape[1] if logits is not None else None
+    if isinstance(k, torch.Tensor) and v is not None:
+        for r, kk in enumerate(k.tolist()):
+            if not (1 <= kk <= v):
+                report.append(f"row {r}: k out of range [1,V] (k={kk}, V={v})")
+    if isinstance(p, torch.Tensor):
+        for r, pp in enumerate(p.tolist()):
+            if not (0.0 < pp <= 1.0):
+                report.append(f"row {r}: p out of range (0,1] (p={pp})")
+    return report
+
+
+def topk_topp(logits: torch.Tensor, k: Union[int, torch.Tensor], p: Union[float, torch.Tensor], *,
+              out: Optional[torch.Tensor] = None, inplace: bool = False,
+              flags: Optional[TruncFlags] = None, sample_size: int = DEFAULT_SAMPLE_SIZE,
+              kept_count: Optional[torch.Tensor] = None, metrics: Optional[torch.Tensor] = None,
+              check: bool = True, stream: Optional[torch.cuda.Stream] = None) -> torch.Tensor:
+    """Exact Top-k then Top-p truncation of a [B, V] CUDA tensor (fp32 or bf16).
+
+    k: int64 per row (k == V disables top-k); p: float64 per row (p == 1 disables top-p).  Returns
+    the masked logits (new tensor, or `logits` itself when inplace).  kept_count (int32 [B]) and
+    metrics (uint8 [B, 40], qrita_row_metrics) are filled when given.  check=True synchronises and
+    raises the reference's ValueError for invalid rows; check=False leaves the call fully async.
+    """
+    if not isinstance(logits, torch.Tensor) or not logits.is_cuda:
+        raise TypeError("logits must be a CUDA tensor (there is no CPU path)")
+    if logits.dim() != 2:
+        raise ValueError("logit batch must be 2-D (rows x vocab)")
+    if logits.dtype not in _DTYPES:
+        raise TypeError(f"unsupported dtype {logits.dtype}; expected float32 or bfloat16")
+    if logits.stride(1) != 1:
+        logits = logits.contiguous()
+    b, v = logits.shape
+    if b == 0 or v == 0:
+        raise ValueError("batch_size and vocab_size must be >= 1")
+    if sample_size < 1:
+        raise ValueError("sample_size must be >= 1")
+    dev = logits.device
+    kt = _per_row(k, b, torch.int64, dev, "k")
+    pt = _per_row(p, b, torch.float64, dev, "p")
+    if inplace:
+        out = logits
+    elif out is None:
+        out = torch.empty_like(logits)
+    elif out.shape != logits.shape or out.dtype != logits.dtype or out.stride(1) != 1:
+        raise ValueError("out must match logits in shape/dtype with unit column stride")
+    fl = (flags or TruncFlags()).bits() | (N.INPLACE if inplace else 0)
+    st = stream or torch.cuda.current_stream(dev)
+    lib = N.load()
+    need = lib.qrita_workspace_bytes(b, v, _DTYPES[logits.dtype], fl)
+    ws = workspace_for(dev, st)
+    with torch.cuda.device(dev):
+        ws_ptr, ws_bytes = ws.get(need, st)
+        rc = lib.qrita_topk_topp(
+            ctypes.c_void_p(logits.data_ptr()), logits.stride(0), _DTYPES[logits.dtype], b, v,
+            ctypes.c_void_p(kt.data_ptr()), ctypes.c_void_p(pt.data_ptr()),
+            ctypes.c_void_p(out.data_ptr()), out.stride(0),
+            ctypes.c_void_p(kept_count.data_ptr() if kept_count is not None else 0),
+            ctypes.c_void_p(metrics.data_ptr() if metrics is not None else 0),
+            ctypes.c_void_p(ws_ptr), ws_bytes, fl, int(sample_size),
+            ctypes.c_void_p(st.cuda_stream))
+        if rc != N.OK:
+            ws.reset()
+            raise RuntimeError(f"qrita_topk_topp failed: {N.strerror(rc)}")
+        if check:
+            check_status(ws_ptr, b, logits, kt, pt, st)
+    return out
+
+
+def metrics_buffer(b: int, device) -> torch.Tensor:
+    return torch.zeros((b, N.METRICS_BYTES), dtype=torch.uint8, device=device)
+
+
+def decode_metrics(buf: torch.Tensor):
+    """uint8 [B, 40] qrita_row_metrics -> list of dicts (host)."""
+    raw = buf.cpu().numpy().tobytes()
+    rows = []
+    sz = N.METRICS_BYTES
+    for i in range(buf.shape[0]):
+        m = N.RowMetricsC.from_buffer_copy(raw[i * sz:(i + 1) * sz])
+        rows.append({f: getattr(m, f) for f, _ in N.RowMetricsC._fields_})
+    return rows

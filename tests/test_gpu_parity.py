@@ -1,0 +1,184 @@
+"""GPU parity: the B200 kernels (through the C ABI) against the reference's golden answers and the
+oracle.  Bar: kept-index sets bit-exact, kept values bit-identical, -inf elsewhere."""
+import numpy as np
+import pytest
+import torch
+
+import paper_2602_01518_b200 as Q
+from oracle.qrita_oracle import oracle_keep_row
+from oracle.synth import to_bf16_bits
+from tests import golden_io as G
+
+pytestmark = pytest.mark.gpu
+
+
+def run(x, k, p, dtype=torch.float32, **flags):
+    xt = torch.from_numpy(np.ascontiguousarray(x)).to("cuda").to(dtype)
+    kt = torch.as_tensor(np.asarray(k, dtype=np.int64), device="cuda")
+    pt = torch.as_tensor(np.asarray(p, dtype=np.float64), device="cuda")
+    kept = torch.zeros(xt.shape[0], dtype=torch.int32, device="cuda")
+    met = Q.ops.metrics_buffer(xt.shape[0], xt.device)
+    out = Q.topk_topp(xt, kt, pt, flags=Q.TruncFlags(**flags) if flags else None, kept_count=kept,
+                      metrics=met)
+    torch.cuda.synchronize()
+    return out.float().cpu().numpy(), kept.cpu().numpy(), Q.ops.decode_metrics(met)
+
+
+def assert_rows(x, got, kept, trip, label):
+    want = G.masked_from_trip(x, trip)
+    same = G.same_bits(got, want)
+    bad = np.nonzero(~same.all(axis=1))[0]
+    assert bad.size == 0, f"{label}: {bad.size} rows differ, first row {bad[0]}"
+    assert np.array_equal(kept, trip[:, 2]), f"{label}: kept counts differ"
+
+
+def test_kats(cuda_device):
+    for row, k, p, keep in G.kats():
+        out, kept, _ = run(row[None, :], [k], [p])
+        want = np.where(keep, row, -np.inf).astype(np.float32)
+        assert G.same_bits(out[0], want).all(), (row[:6], k, p, out[0][:6])
+        assert kept[0] == keep.sum()
+
+
+def test_signed_zero_bits_preserved(cuda_device):
+    row = np.array([-0.0, 0.0, -0.0, 1.0, -0.0], dtype=np.float32)
+    out, kept, _ = run(row[None, :], [3], [1.0])
+    assert out[0].view(np.uint32).tolist()[:2] == [0x80000000, 0]
+    assert np.isneginf(out[0][2]) and kept[0] == 3
+
+
+def test_exhaustive_small_rows(cuda_device):
+    z = G.exhaustive()
+    vlen = z["vlen"]
+    for v in np.unique(vlen):
+        sel = np.nonzero(vlen == v)[0]
+        x = np.ascontiguousarray(z["rows"][sel, :v])
+        trip = np.stack([z["zb"][sel], z["cut"][sel], z["count"][sel]], axis=1).astype(np.int64)
+        out, kept, _ = run(x, z["k"][sel], z["p"][sel])
+        assert_rows(x, out, kept, trip, f"V={v}")
+
+
+def test_acceptance_corpus_and_metrics(cuda_device):
+    for key, x, k, p, trip, mets in G.corpus():
+        out, kept, met = run(x, k, p)
+        assert_rows(x, out, kept, trip, key)
+        hit = np.array([m["trunc_hit"] for m in met])
+        cnt = np.array([m["outlier_count"] for m in met])
+        # reference RowMetrics parity: same sigma threshold -> same outlier counts and hit flags
+        assert np.array_equal(cnt, mets["outlier_count"]), key
+        assert np.array_equal(hit, mets["trunc_hit"].astype(bool)), key
+
+
+@pytest.mark.parametrize("flags", [
+    dict(search="binary"), dict(use_sigma_trunc=False), dict(force_fallback=True),
+])
+def test_ablation_flags_same_output(cuda_device, flags):
+    for key, x, k, p, trip, _ in G.corpus():
+        if x.shape[1] not in (8, 1000, 32768):
+            continue
+        out, kept, _ = run(x, k, p, **flags)
+        assert_rows(x, out, kept, trip, f"{key} {flags}")
+
+
+@pytest.mark.parametrize("name", ["cfg1", "cfg2", "cfg3", "cfg4", "cfg5"])
+def test_configs_full_size(cuda_device, name):
+    x, k, p, dtype, trip, mets = G.config(name)
+    tdt = torch.bfloat16 if dtype == "bf16" else torch.float32
+    out, kept, met = run(x, k, p, dtype=tdt)
+    assert_rows(x, out, kept, trip, name)
+    n = mets["outlier_count"].shape[0]
+    assert np.array_equal(np.array([m["outlier_count"] for m in met[:n]]), mets["outlier_count"]), name
+    assert np.array_equal(np.array([m["trunc_hit"] for m in met[:n]]), mets["trunc_hit"].astype(bool)), name
+
+
+def test_bf16_output_bits(cuda_device):
+    x, k, p, dtype, trip, _ = G.config("cfg3")
+    xb = torch.from_numpy(to_bf16_bits(x[:4]).view(np.int16)).to("cuda").view(torch.bfloat16)
+    out = Q.topk_topp(xb, torch.as_tensor(k[:4], device="cuda"), torch.as_tensor(p[:4], device="cuda"))
+    ob = out.view(torch.int16).cpu().numpy().view(np.uint16)
+    keep = np.stack([G.keep_from_trip(x[i], trip[i]) for i in range(4)])
+    want = np.where(keep, to_bf16_bits(x[:4]), np.uint16(0xFF80))
+    assert np.array_equal(ob, want)
+
+
+def test_determinism_and_inplace(cuda_device):
+    x, k, p, _, trip, _ = G.config("cfg2")
+    xt = torch.from_numpy(x[:64]).cuda()
+    kt, pt = torch.as_tensor(k[:64], device="cuda"), torch.as_tensor(p[:64], device="cuda")
+    a = Q.topk_topp(xt, kt, pt)
+    for _ in range(3):
+        b = Q.topk_topp(xt, kt, pt)
+        assert torch.equal(a.view(torch.int32), b.view(torch.int32))
+    y = xt.clone()
+    Q.topk_topp(y, kt, pt, inplace=True)
+    assert torch.equal(a.view(torch.int32), y.view(torch.int32))
+
+
+def test_random_ties_and_extremes(cuda_device):
+    rng = np.random.default_rng(123)
+    rows, ks, ps = [], [], []
+    v = 3000
+    for i in range(48):
+        kind = i % 4
+        if kind == 0:
+            r = rng.integers(-3, 4, size=v).astype(np.float32)       # massive ties
+        elif kind == 1:
+            r = (rng.normal(size=v) * 40).astype(np.float32)          # wide spread, underflowing exp
+        elif kind == 2:
+            r = np.full(v, 2.5, np.float32)                            # all equal
+        else:
+            r = rng.normal(size=v).astype(np.float32) * 1e-30         # tiny logits
+        rows.append(r)
+        ks.append(int(rng.integers(1, v + 1)))
+        ps.append(float(rng.choice([1e-12, 0.3, 0.9, 0.999999, 1.0])))
+    x = np.stack(rows)
+    out, kept, _ = run(x, ks, ps)
+    for i in range(x.shape[0]):
+        keep = oracle_keep_row(x[i], ks[i], ps[i])
+        want = np.where(keep, x[i], -np.inf).astype(np.float32)
+        assert G.same_bits(out[i], want).all(), (i, ks[i], ps[i])
+        assert kept[i] == keep.sum()
+
+
+def test_run_batch_dropin_numpy(cuda_device):
+    batch = Q.synth_batch("gaussian", 16, 2048, seed=0)
+    targets = Q.TruncTargets.uniform(16, 25, 0.9)
+    out, rep = Q.run_batch(batch, targets, Q.EngineConfig())
+    assert isinstance(out, np.ndarray) and out.dtype == np.float32
+    want, _ = __import__("oracle.qrita_oracle", fromlist=["oracle_batch"]).oracle_batch(batch.values, 25, 0.9)
+    assert G.same_bits(out, want).all()
+    assert rep.hit_rate == 1.0 and len(rep.per_row) == 16
+    with pytest.raises(ValueError, match="non-finite"):
+        vals = np.zeros((2, 8), dtype=np.float32)
+        vals[0, 0] = np.inf
+        Q.run_batch(Q.LogitBatch(vals), Q.TruncTargets.uniform(2, 4, 1.0), Q.EngineConfig())
+
+
+def test_device_side_nonfinite_status(cuda_device):
+    x = torch.randn(3, 5000, device="cuda")
+    x[1, 1234] = float("nan")
+    with pytest.raises(ValueError, match="NaN logit at row 1, col 1234"):
+        Q.topk_topp(x, 10, 0.9)
+    with pytest.raises(ValueError, match="k out of range"):
+        Q.topk_topp(torch.randn(2, 100, device="cuda"), torch.tensor([5, 101], device="cuda"), 0.5)
+
+
+def test_pipeline_row_api(cuda_device):
+    out = Q.truncate_topk(np.array([5, 5, 3, 5, 1], dtype=np.float32), 2)
+    assert out.masked_row.tolist()[:2] == [5, 5] and out.kept_count == 2
+    out = Q.truncate_topp(np.array([2, 1, 0], dtype=np.float32), 0.7)
+    assert np.isneginf(out.masked_row[2]) and out.kept_count == 2
+    row = np.array([3, 2, 1, 0], dtype=np.float32)
+    res = Q.truncate_topk(row, 2, inplace=True)
+    assert res.masked_row is row and np.isneginf(row[3])
+    assert Q.truncate_topk(np.array([5, 5, 3, 5, 1], dtype=np.float32), 2, dup_handling=False).kept_count == 3
+    with pytest.raises(ValueError):
+        Q.truncate_topk(np.zeros(4, dtype=np.float32), 5)
+    with pytest.raises(ValueError):
+        Q.truncate_topp(np.zeros(4, dtype=np.float32), 1.5)
+
+
+def test_verify_batch_with_exact_sort(cuda_device):
+    batch = Q.synth_batch("quantized", 16, 512, seed=3, g=8)
+    targets = Q.TruncTargets(np.arange(1, 17) * 7, np.linspace(0.3, 0.99, 16))
+    assert Q.verify_batch(batch, targets, Q.EngineConfig()) == []
