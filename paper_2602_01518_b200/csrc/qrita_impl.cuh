@@ -268,6 +268,7 @@ __global__ void __launch_bounds__(256) qrita_prep(Params P) {
     P.plans[row] = pl;
     P.status[row] = (bad_k ? ST_BAD_K : 0) | (bad_p ? ST_BAD_P : 0);
     P.nf_col[row] = -1;
+    P.row_done[row] = 0u;  // the layout moves with B, so counters are reset here, every call
   }
 }
 
@@ -1033,29 +1034,35 @@ __global__ void __launch_bounds__(kThreads, 2) qrita_main(Params P) {
     }
     __syncthreads();
     // ---- outliers -> per-chunk HBM scratch, index order (order-stable compaction, gather_outliers)
+    // Within a (slot, warp) segment the index order is lane-major: element (lane, w) sits at
+    // 4*lane + w (8*lane + w for bf16), so its rank = outliers of lower lanes + my earlier w.
     if (gather) {
       const size_t slot = ((size_t)row * nch + c) * kCapChunk;
       const uint32_t lt = (1u << lane) - 1u;
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const int ebase = (u * kThreads + tid) * W;
-        uint32_t pos = ms.woff[u][warp];
+        uint32_t b[W];
+        uint32_t mine = 0u, lower = 0u;
 #pragma unroll
         for (int w = 0; w < W; ++w) {
-          uint32_t b = 0u;
-          if (VEC) b = lane_bits<T>(v[u], w);
-          else if (ebase + w < n) b = Elem<T>::bits(src[ebase + w]);
-          const bool cand = (ebase + w < n) && key_of_bits(b) >= key_thr;
-          const uint32_t bal = __ballot_sync(0xffffffffu, cand);
-          // elements before mine in this slot: lanes below me (all w) + my earlier w
-          if (cand) {
-            uint32_t q = pos + (uint32_t)__popc(bal & lt);
+          b[w] = 0u;
+          if (VEC) b[w] = lane_bits<T>(v[u], w);
+          else if (ebase + w < n) b[w] = Elem<T>::bits(src[ebase + w]);
+          const bool cand = (ebase + w < n) && key_of_bits(b[w]) >= key_thr;
+          mine |= cand ? (1u << w) : 0u;
+          lower += (uint32_t)__popc(__ballot_sync(0xffffffffu, cand) & lt);
+        }
+        uint32_t q = ms.woff[u][warp] + lower;
+#pragma unroll
+        for (int w = 0; w < W; ++w) {
+          if ((mine >> w) & 1u) {
             if (q < (uint32_t)kCapChunk) {
-              P.cand_bits[slot + q] = b;
+              P.cand_bits[slot + q] = b[w];
               P.cand_idx[slot + q] = (uint32_t)(c0 + ebase + w);
             }
+            ++q;
           }
-          pos += (uint32_t)__popc(bal);
         }
       }
     }

@@ -90,6 +90,11 @@ def _per_row(x, b: int, dtype: torch.dtype, device: torch.device, name: str) -> 
     return torch.full((b,), x, dtype=dtype, device=device)
 
 
+def _row_stride(t: torch.Tensor) -> int:
+    # a size-1 batch dimension may carry any stride (numpy/torch relaxed strides)
+    return t.stride(0) if t.shape[0] > 1 else t.shape[1]
+
+
 class TruncationError(ValueError):
     """Raised with the reference's ValueError wording (core.py:126-139)."""
 
@@ -148,7 +153,7 @@ def topk_topp(logits: torch.Tensor, k: Union[int, torch.Tensor], p: Union[float,
         raise ValueError("logit batch must be 2-D (rows x vocab)")
     if logits.dtype not in _DTYPES:
         raise TypeError(f"unsupported dtype {logits.dtype}; expected float32 or bfloat16")
-    if logits.stride(1) != 1:
+    if logits.stride(1) != 1 or (logits.shape[0] > 1 and logits.stride(0) < logits.shape[1]):
         logits = logits.contiguous()
     b, v = logits.shape
     if b == 0 or v == 0:
@@ -172,9 +177,9 @@ def topk_topp(logits: torch.Tensor, k: Union[int, torch.Tensor], p: Union[float,
     with torch.cuda.device(dev):
         ws_ptr, ws_bytes = ws.get(need, st)
         rc = lib.qrita_topk_topp(
-            ctypes.c_void_p(logits.data_ptr()), logits.stride(0), _DTYPES[logits.dtype], b, v,
+            ctypes.c_void_p(logits.data_ptr()), _row_stride(logits), _DTYPES[logits.dtype], b, v,
             ctypes.c_void_p(kt.data_ptr()), ctypes.c_void_p(pt.data_ptr()),
-            ctypes.c_void_p(out.data_ptr()), out.stride(0),
+            ctypes.c_void_p(out.data_ptr()), _row_stride(out),
             ctypes.c_void_p(kept_count.data_ptr() if kept_count is not None else 0),
             ctypes.c_void_p(metrics.data_ptr() if metrics is not None else 0),
             ctypes.c_void_p(ws_ptr), ws_bytes, fl, int(sample_size),

@@ -1,0 +1,54 @@
+"""Diagnostics: run small cases on the GPU and print mismatches against the oracle."""
+import sys, os
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np, torch
+import paper_2602_01518_b200 as Q
+from oracle.qrita_oracle import oracle_keep_row
+
+def run(x, k, p, **fl):
+    xt = torch.from_numpy(np.ascontiguousarray(x)).cuda()
+    kt = torch.as_tensor(np.asarray(k, np.int64), device="cuda"); pt = torch.as_tensor(np.asarray(p, np.float64), device="cuda")
+    kept = torch.zeros(x.shape[0], dtype=torch.int32, device="cuda")
+    met = Q.ops.metrics_buffer(x.shape[0], xt.device)
+    out = Q.topk_topp(xt, kt, pt, kept_count=kept, metrics=met, flags=Q.TruncFlags(**fl) if fl else None)
+    return out.cpu().numpy(), kept.cpu().numpy(), Q.ops.decode_metrics(met)
+
+def check(name, x, k, p, maxshow=4, **fl):
+    out, kept, met = run(x, k, p, **fl)
+    nbad = 0
+    for i in range(x.shape[0]):
+        keep = oracle_keep_row(x[i], int(k[i]), float(p[i]))
+        got = ~np.isneginf(out[i])
+        if not np.array_equal(got, keep) or kept[i] != keep.sum():
+            nbad += 1
+            if nbad <= maxshow:
+                print(f"  [{name}] row {i} V={x.shape[1]} k={k[i]} p={p[i]!r} want {keep.sum()} got {got.sum()} kept_count {kept[i]}")
+                print(f"     met {met[i]}")
+                if x.shape[1] <= 16:
+                    print("     row", x[i].tolist(), "want", keep.astype(int).tolist(), "got", got.astype(int).tolist())
+    print(f"{name}: {nbad}/{x.shape[0]} bad")
+
+rng = np.random.default_rng(0)
+# 1. tiny top-p rows
+x = np.array([[2,1,0,0],[0,0,0,0],[9,0,0,0],[1,2,3,4]], np.float32)
+check("tiny-topp", x, [4]*4, [0.7,0.5,0.5,0.9])
+check("tiny-topk", x, [2]*4, [1.0]*4)
+check("tiny-comb", x, [3]*4, [0.9]*4)
+x = rng.normal(size=(16, 1000)).astype(np.float32)
+check("g1000-topp", x, [1000]*16, rng.uniform(0.1, 0.99, 16))
+check("g1000-topk", x, rng.integers(1, 1000, 16), [1.0]*16)
+check("g1000-comb", x, rng.integers(1, 1000, 16), rng.uniform(0.1, 0.99, 16))
+check("g1000-topp-nosigma", x, [1000]*16, rng.uniform(0.1, 0.99, 16), use_sigma_trunc=False)
+check("g1000-topk-nosigma", x, rng.integers(1, 1000, 16), [1.0]*16, use_sigma_trunc=False)
+x = rng.normal(size=(8, 40000)).astype(np.float32)
+check("g40000-topp", x, [40000]*8, rng.uniform(0.5, 0.99, 8))
+check("g40000-comb", x, rng.integers(1, 1024, 8), rng.uniform(0.5, 0.99, 8))
+check("g40000-comb-ff", x, rng.integers(1, 1024, 8), rng.uniform(0.5, 0.99, 8), force_fallback=True)
+xq = np.round(rng.normal(size=(8, 3000))*2).astype(np.float32)
+check("q3000-topk", xq, rng.integers(1, 3000, 8), [1.0]*8)
+check("q3000-topp", xq, [3000]*8, rng.uniform(0.1, 0.99, 8))
+# exhaustive-like for top-k V=5
+import itertools
+rows = np.array(list(itertools.product((0.,1.,2.), repeat=5)), np.float32)
+for kk in range(1, 6):
+    check(f"exh5-k{kk}", rows, [kk]*len(rows), [1.0]*len(rows), maxshow=2)
