@@ -52,7 +52,7 @@ enum {
   QRITA_FORCE_FALLBACK  = 1 << 2, /* force_fallback=True: gather, but search the full row           */
   QRITA_NO_DUP          = 1 << 3, /* duplication_handling_enabled=False: keep whole boundary cluster*/
   QRITA_INPLACE         = 1 << 4, /* out == logits (pipeline.py:72-74)                               */
-  QRITA_WIDE_SEARCH     = 1 << 5  /* 15 pivots per pass (B200 extension; same output)               */
+  QRITA_RESERVED_5      = 1 << 5  /* reserved (rejected)                                            */
 };
 
 /* return codes */
@@ -105,6 +105,16 @@ int qrita_topk_topp(const void *logits, int64_t ld_in, int dtype, int B, int V,
                     int32_t *kept_count, qrita_row_metrics *metrics,
                     void *workspace, size_t ws_bytes, int flags, int sample_size,
                     qrita_stream_t stream);
+
+/* Same as qrita_topk_topp; additionally records `prep_done_event` (a cudaEvent_t, may be NULL) on
+ * `stream` between the per-row preparation kernel and the streaming/search kernel, so a caller can
+ * time the two launches separately with events (bench.py's roofline measurement). */
+int qrita_topk_topp_ex(const void *logits, int64_t ld_in, int dtype, int B, int V,
+                       const int64_t *k, const double *p,
+                       void *out, int64_t ld_out,
+                       int32_t *kept_count, qrita_row_metrics *metrics,
+                       void *workspace, size_t ws_bytes, int flags, int sample_size,
+                       qrita_stream_t stream, void *prep_done_event);
 
 /* Synchronises `stream`, then reports the first failing row of the last call on this workspace:
  * returns QRITA_OK or QRITA_EINVAL_K / QRITA_EINVAL_P / QRITA_ENONFINITE, and fills *row / *col

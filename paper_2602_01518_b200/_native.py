@@ -31,7 +31,8 @@ ECUDA = 6
 ENCCL = 7
 
 EXPORTED_SYMBOLS = (
-    "qrita_workspace_bytes", "qrita_workspace_init", "qrita_topk_topp", "qrita_get_status",
+    "qrita_workspace_bytes", "qrita_workspace_init", "qrita_topk_topp", "qrita_topk_topp_ex",
+    "qrita_get_status",
     "qrita_strerror", "qrita_version",
 )
 
@@ -78,6 +79,9 @@ def load() -> ctypes.CDLL:
     lib.qrita_workspace_init.restype = i32
     lib.qrita_topk_topp.argtypes = [vp, i64, i32, i32, i32, vp, vp, vp, i64, vp, vp, vp, sz, i32, i32, vp]
     lib.qrita_topk_topp.restype = i32
+    lib.qrita_topk_topp_ex.argtypes = [vp, i64, i32, i32, i32, vp, vp, vp, i64, vp, vp, vp, sz, i32, i32,
+                                       vp, vp]
+    lib.qrita_topk_topp_ex.restype = i32
     lib.qrita_get_status.argtypes = [vp, i32, ctypes.POINTER(i32), ctypes.POINTER(i32), vp]
     lib.qrita_get_status.restype = i32
     lib.qrita_strerror.argtypes = [i32]

@@ -2,5 +2,7 @@
 #include "qrita_impl.cuh"
 
 namespace qrita {
-cudaError_t launch_bf16(const Params &P, cudaStream_t st, bool vec) { return launch_all<uint16_t>(P, st, vec); }
+cudaError_t launch_bf16(const Params &P, cudaStream_t st, bool vec, cudaEvent_t prep_done) {
+  return launch_all<uint16_t>(P, st, vec, prep_done);
+}
 }  // namespace qrita

@@ -4,12 +4,73 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include <algorithm>
+#include <vector>
+
 #include "qrita_types.cuh"
 
 // ================================================================================================
 // C ABI (include/qrita_b200.h)
 // ================================================================================================
 using namespace qrita;
+
+namespace {
+
+struct PwNode {
+  int off, len, height, left, right;
+};
+
+// Builds numpy's pairwise tree (leaf: len <= 128; split n2 = n/2 rounded down to a multiple of 8).
+int pw_build(int off, int len, std::vector<PwNode> &leaves, std::vector<PwNode> &inner) {
+  if (len <= 128) {
+    leaves.push_back(PwNode{off, len, 0, -1, -1});
+    return (int)leaves.size() - 1;          // leaf ids are provisional: leaves are numbered in order
+  }
+  int n2 = len / 2;
+  n2 -= n2 % 8;
+  const int l = pw_build(off, n2, leaves, inner);
+  const bool l_leaf = n2 <= 128;
+  const int r = pw_build(off + n2, len - n2, leaves, inner);
+  const bool r_leaf = (len - n2) <= 128;
+  const int hl = l_leaf ? 0 : inner[l].height, hr = r_leaf ? 0 : inner[r].height;
+  inner.push_back(PwNode{off, len, 1 + (hl > hr ? hl : hr), l_leaf ? l : -2 - l, r_leaf ? r : -2 - r});
+  return (int)inner.size() - 1;
+}
+
+void pw_tree(int n, PwTree &t) {
+  memset(&t, 0, sizeof(t));
+  t.n = n;
+  if (n > kPwStage) return;
+  std::vector<PwNode> leaves, inner;
+  pw_build(0, n, leaves, inner);
+  if ((int)leaves.size() > kPwMaxLeaves) return;
+  const int nl = (int)leaves.size();
+  // order internal nodes by height (stable) and assign ids nl + position
+  std::vector<int> order(inner.size());
+  for (size_t i = 0; i < inner.size(); ++i) order[i] = (int)i;
+  std::stable_sort(order.begin(), order.end(),
+                   [&](int a, int b) { return inner[a].height < inner[b].height; });
+  std::vector<int> id_of(inner.size());
+  for (size_t pos = 0; pos < order.size(); ++pos) id_of[order[pos]] = nl + (int)pos;
+  auto child_id = [&](int c) { return c >= 0 ? c : id_of[-2 - c]; };
+  for (int i = 0; i < nl; ++i) {
+    t.leaf_off[i] = (uint16_t)leaves[i].off;
+    t.leaf_len[i] = (uint16_t)leaves[i].len;
+  }
+  int levels = 0;
+  for (size_t pos = 0; pos < order.size(); ++pos) {
+    const PwNode &nd = inner[order[pos]];
+    t.left[pos] = (uint8_t)child_id(nd.left);
+    t.right[pos] = (uint8_t)child_id(nd.right);
+    if (nd.height > levels) levels = nd.height;
+    t.level_end[nd.height - 1] = (uint8_t)(pos + 1);
+  }
+  t.n_leaves = (int16_t)nl;
+  t.n_internal = (int16_t)inner.size();
+  t.n_levels = (int16_t)levels;
+}
+
+}  // namespace
 
 extern "C" {
 
@@ -29,6 +90,15 @@ int qrita_topk_topp(const void *logits, int64_t ld_in, int dtype, int B, int V,
                     int32_t *kept_count, qrita_row_metrics *metrics,
                     void *workspace, size_t ws_bytes, int flags, int sample_size,
                     qrita_stream_t stream) {
+  return qrita_topk_topp_ex(logits, ld_in, dtype, B, V, k, p, out, ld_out, kept_count, metrics,
+                            workspace, ws_bytes, flags, sample_size, stream, NULL);
+}
+
+int qrita_topk_topp_ex(const void *logits, int64_t ld_in, int dtype, int B, int V,
+                       const int64_t *k, const double *p, void *out, int64_t ld_out,
+                       int32_t *kept_count, qrita_row_metrics *metrics,
+                       void *workspace, size_t ws_bytes, int flags, int sample_size,
+                       qrita_stream_t stream, void *prep_done_event) {
   if (!logits || !out || !k || !p || !workspace) return QRITA_EINVAL_ARG;
   if (B < 1 || V < 1 || ld_in < V || ld_out < V || sample_size < 1) return QRITA_EINVAL_ARG;
   if (dtype != QRITA_DTYPE_F32 && dtype != QRITA_DTYPE_BF16) return QRITA_EINVAL_ARG;
@@ -52,19 +122,18 @@ int qrita_topk_topp(const void *logits, int64_t ld_in, int dtype, int B, int V,
   P.cstats = (ChunkStat *)(ws + L.cstats);
   P.cand_bits = (uint32_t *)(ws + L.cand_bits);
   P.cand_idx = (uint32_t *)(ws + L.cand_idx);
-  P.row_done = (uint32_t *)(ws + L.row_done);
-  P.work_ctr = (uint32_t *)(ws + L.ctrs);
-  P.exit_ctr = (uint32_t *)(ws + L.ctrs + 4);
   P.status = (int32_t *)(ws + L.status);
   P.nf_col = (int32_t *)(ws + L.nf_col);
   P.nchunks = (int)nchunks;
   P.total_items = (int)((size_t)B * nchunks);
+  pw_tree(sample_size < V ? sample_size : V, P.tree);
 
   const size_t es = dtype == QRITA_DTYPE_F32 ? 4 : 2;
   const bool vec = ((uintptr_t)logits % 16 == 0) && ((uintptr_t)out % 16 == 0) &&
                    ((size_t)ld_in * es % 16 == 0) && ((size_t)ld_out * es % 16 == 0);
-  cudaError_t e = dtype == QRITA_DTYPE_F32 ? launch_f32(P, (cudaStream_t)stream, vec)
-                                           : launch_bf16(P, (cudaStream_t)stream, vec);
+  cudaError_t e = dtype == QRITA_DTYPE_F32
+                      ? launch_f32(P, (cudaStream_t)stream, vec, (cudaEvent_t)prep_done_event)
+                      : launch_bf16(P, (cudaStream_t)stream, vec, (cudaEvent_t)prep_done_event);
   return e == cudaSuccess ? QRITA_OK : QRITA_ECUDA;
 }
 

@@ -13,7 +13,7 @@
 
 namespace qrita {
 
-constexpr int kThreads = 512;
+constexpr int kThreads = 256;  // row-tail CTA size
 constexpr int kWarps = kThreads / 32;
 constexpr uint32_t kNoCut = 0xffffffffu;
 
@@ -173,6 +173,14 @@ __device__ __forceinline__ Fx fx_round_threshold(double p) {
   unsigned long long pb = (unsigned long long)__double_as_longlong(p);
   bool even = (pb & 1ull) == 0ull;
   return even ? mid : fx_add_unit(mid);
+}
+
+// ------------------------------------------------------------------------------------------------
+// Programmatic dependent launch (griddepcontrol, sm_90+)
+// ------------------------------------------------------------------------------------------------
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 
 // ------------------------------------------------------------------------------------------------

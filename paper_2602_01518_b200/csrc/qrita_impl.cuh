@@ -169,13 +169,12 @@ __device__ double pairwise_tree(int n, LeafFn leaf) {
 
 template <typename T>
 __global__ void __launch_bounds__(256) qrita_prep(Params P) {
-  __shared__ int s_off[kMaxLeaves];
-  __shared__ int s_len[kMaxLeaves];
-  __shared__ double s_sum[kMaxLeaves];
-  __shared__ double s_sq[kMaxLeaves];
-  __shared__ int s_nl;
+  __shared__ float s_x[kPwStage];
+  __shared__ double s_acc[2][kPwMaxLeaves][8];
+  __shared__ double s_val[2][2 * kPwMaxLeaves];
   __shared__ double s_res[2];
 
+  pdl_launch_dependents();  // the streaming kernel may start loading logits right away
   const int row = blockIdx.x;
   const int tid = threadIdx.x;
   const int V = P.V;
@@ -196,33 +195,66 @@ __global__ void __launch_bounds__(256) qrita_prep(Params P) {
   uint32_t key_thr = 0xffffffffu;
   if (want_thr) {  // uniform per block
     const T *a = (const T *)P.logits + (size_t)row * P.ld_in;
-    const int n = min(P.sample_size, V);
-    if (tid == 0) {
-      int nl = 0;
-      pairwise_tree(n, [&](int o, int m) -> double {
-        if (nl < kMaxLeaves) { s_off[nl] = o; s_len[nl] = m; }
-        ++nl;
-        return 0.0;
-      });
-      s_nl = nl;
-    }
-    __syncthreads();
-    const int nl = s_nl;
-    if (nl <= kMaxLeaves) {
-      for (int i = tid; i < nl; i += blockDim.x) {
-        s_sum[i] = leaf_sum<T, false>(a + s_off[i], s_len[i]);
-        s_sq[i] = leaf_sum<T, true>(a + s_off[i], s_len[i]);
+    const PwTree &tr = P.tree;
+    const int n = tr.n;
+    const int nl = tr.n_leaves;
+    if (nl > 0) {
+      for (int i = tid; i < n; i += blockDim.x) s_x[i] = __uint_as_float(Elem<T>::bits(a[i]));
+      __syncthreads();
+      // numpy's 8-accumulator leaf loop, one thread per (leaf, accumulator)
+      for (int q = tid; q < nl * 8; q += blockDim.x) {
+        const int L = q >> 3, j = q & 7;
+        const int o = tr.leaf_off[L], m = tr.leaf_len[L];
+        if (m >= 8) {
+          double r0 = (double)s_x[o + j];
+          double r1 = __dmul_rn(r0, r0);
+          for (int i = 8; i < m - (m % 8); i += 8) {
+            const double x = (double)s_x[o + i + j];
+            r0 = __dadd_rn(r0, x);
+            r1 = __dadd_rn(r1, __dmul_rn(x, x));
+          }
+          s_acc[0][L][j] = r0;
+          s_acc[1][L][j] = r1;
+        }
       }
       __syncthreads();
-      if (tid == 0) {
-        int c = 0;
-        s_res[0] = pairwise_tree(n, [&](int, int) -> double { return s_sum[c++]; });
-        c = 0;
-        s_res[1] = pairwise_tree(n, [&](int, int) -> double { return s_sq[c++]; });
+      for (int q = tid; q < nl * 2; q += blockDim.x) {
+        const int L = q >> 1, sq = q & 1;
+        const int o = tr.leaf_off[L], m = tr.leaf_len[L];
+        double res;
+        int i;
+        if (m < 8) {
+          res = 0.0;
+          i = 0;
+        } else {
+          const double *r = s_acc[sq][L];
+          res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                          __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+          i = m - (m % 8);
+        }
+        for (; i < m; ++i) {
+          const double x = (double)s_x[o + i];
+          res = __dadd_rn(res, sq ? __dmul_rn(x, x) : x);
+        }
+        s_val[sq][L] = res;
       }
-    } else if (tid == 0) {  // very long samples: serial replay
-      s_res[0] = pairwise_tree(n, [&](int o, int m) -> double { return leaf_sum<T, false>(a + o, m); });
-      s_res[1] = pairwise_tree(n, [&](int o, int m) -> double { return leaf_sum<T, true>(a + o, m); });
+      __syncthreads();
+      // internal nodes level by level: pw(a, n) = pw(a, n2) + pw(a + n2, n - n2)
+      int lo = 0;
+      for (int h = 0; h < tr.n_levels; ++h) {
+        const int hi = tr.level_end[h];
+        for (int q = lo + (tid >> 1); q < hi; q += blockDim.x >> 1) {
+          const int sq = tid & 1;
+          s_val[sq][nl + q] = __dadd_rn(s_val[sq][tr.left[q]], s_val[sq][tr.right[q]]);
+        }
+        lo = hi;
+        __syncthreads();
+      }
+      if (tid < 2) s_res[tid] = s_val[tid][nl + tr.n_internal - 1 < nl ? 0 : nl + tr.n_internal - 1];
+    } else if (tid < 2) {  // long samples (non-default sample_size): serial replay from global
+      s_res[tid] = tid == 0
+          ? pairwise_tree(n, [&](int o, int m) -> double { return leaf_sum<T, false>(a + o, m); })
+          : pairwise_tree(n, [&](int o, int m) -> double { return leaf_sum<T, true>(a + o, m); });
     }
     __syncthreads();
     const double sum = s_res[0], sq = s_res[1];
@@ -268,17 +300,33 @@ __global__ void __launch_bounds__(256) qrita_prep(Params P) {
     P.plans[row] = pl;
     P.status[row] = (bad_k ? ST_BAD_K : 0) | (bad_p ? ST_BAD_P : 0);
     P.nf_col[row] = -1;
-    P.row_done[row] = 0u;  // the layout moves with B, so counters are reset here, every call
   }
 }
 
 // ------------------------------------------------------------------------------------------------
 // Row tail: search + masking, executed by one whole CTA
 // ------------------------------------------------------------------------------------------------
+// Pivot-search state, owned by warp 0 and broadcast through shared memory.
+struct SearchState {
+  uint32_t l, r, cl, cr;
+  uint32_t done, K, n_gt, n_eq;
+  int iters, pad;
+  Fx Ml, Mr, H;
+};
+
 struct TailSmem {
-  uint32_t red_u[kWarps][48];  // per-warp partials
-  uint32_t res_u[48];          // block result
-  uint32_t u[8];               // broadcast scalars
+  uint32_t red[2][kWarps][48];  // double-buffered per-warp partials of the block reductions
+  uint32_t sel[kWarps];         // per-warp counts of select_nth_eq
+  uint32_t u[8];                // broadcast scalars
+  SearchState st;
+};
+
+// Block-reduction context.  `par` is block-uniform: consecutive reductions alternate between the
+// two partial buffers, so each reduction needs a single barrier.
+struct Red {
+  TailSmem &sm;
+  int par;
+  __device__ explicit Red(TailSmem &s) : sm(s), par(0) {}
 };
 
 // Element sources: i -> (fp32 bits, index)
@@ -331,48 +379,47 @@ __device__ __forceinline__ void bk_add(Buckets<NP, MASS> &b, const uint32_t *piv
   }
 }
 
-// Block reduction; result in sm.res_u = [cnt(NP) | mn(NP) | mc(NP) | 12 mass pieces per bucket].
+// Block reduction in place: on return every thread holds the block totals in `b`.
+// Warp stage with redux.sync, one barrier, then every warp reduces the 16 warp partials itself.
 template <int NP, bool MASS>
-__device__ void bk_reduce(const Buckets<NP, MASS> &b, TailSmem &sm) {
+__device__ void bk_reduce(Buckets<NP, MASS> &b, Red &R) {
   constexpr int NV = 3 * NP + (MASS ? 12 * NP : 0);
   static_assert(NV <= 48, "reduction scratch too small");
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t(*red)[48] = R.sm.red[R.par];
+  R.par ^= 1;
 #pragma unroll
   for (int j = 0; j < NP; ++j) {
     const uint32_t c = warp_sum(b.cnt[j]);
     const uint32_t m = warp_min(b.mn[j]);
     const uint32_t mc = warp_sum(b.mn[j] == m ? b.mc[j] : 0u);
-    if (lane == 0) { sm.red_u[warp][j] = c; sm.red_u[warp][NP + j] = m; sm.red_u[warp][2 * NP + j] = mc; }
+    if (lane == 0) { red[warp][j] = c; red[warp][NP + j] = m; red[warp][2 * NP + j] = mc; }
     if (MASS) {
       uint32_t q[12];
       fx_split(b.ms[j], q);
 #pragma unroll
       for (int i = 0; i < 12; ++i) {
-        const uint32_t s = warp_sum(q[i]);
-        if (lane == 0) sm.red_u[warp][3 * NP + 12 * j + i] = s;
+        const uint32_t sum = warp_sum(q[i]);
+        if (lane == 0) red[warp][3 * NP + 12 * j + i] = sum;
       }
     }
   }
   __syncthreads();
-  if (warp == 0) {
-    const bool act = lane < kWarps;
+  const bool act = lane < kWarps;
 #pragma unroll
-    for (int j = 0; j < NP; ++j) {
-      const uint32_t c = warp_sum(act ? sm.red_u[lane][j] : 0u);
-      const uint32_t mv = act ? sm.red_u[lane][NP + j] : 0xffffffffu;
-      const uint32_t m = warp_min(mv);
-      const uint32_t mc = warp_sum((act && mv == m) ? sm.red_u[lane][2 * NP + j] : 0u);
-      if (lane == 0) { sm.res_u[j] = c; sm.res_u[NP + j] = m; sm.res_u[2 * NP + j] = mc; }
-      if (MASS) {
+  for (int j = 0; j < NP; ++j) {
+    b.cnt[j] = warp_sum(act ? red[lane][j] : 0u);
+    const uint32_t mv = act ? red[lane][NP + j] : 0xffffffffu;
+    const uint32_t m = warp_min(mv);
+    b.mn[j] = m;
+    b.mc[j] = warp_sum((act && mv == m) ? red[lane][2 * NP + j] : 0u);
+    if (MASS) {
+      uint32_t q[12];
 #pragma unroll
-        for (int i = 0; i < 12; ++i) {
-          const uint32_t s = warp_sum(act ? sm.red_u[lane][3 * NP + 12 * j + i] : 0u);
-          if (lane == 0) sm.res_u[3 * NP + 12 * j + i] = s;
-        }
-      }
+      for (int i = 0; i < 12; ++i) q[i] = warp_sum(act ? red[lane][3 * NP + 12 * j + i] : 0u);
+      b.ms[j] = fx_join(q);
     }
   }
-  __syncthreads();
 }
 
 template <int NP>
@@ -389,16 +436,67 @@ struct KRes {
   int iters;
 };
 
+// Warp stage of a pivot pass: lane 0 of every warp stores the warp's bucket partials.
+template <int NP, bool MASS>
+__device__ __forceinline__ void bk_warp_partials(const Buckets<NP, MASS> &b, uint32_t (*red)[48]) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int j = 0; j < NP; ++j) {
+    const uint32_t c = warp_sum(b.cnt[j]);
+    const uint32_t m = warp_min(b.mn[j]);
+    const uint32_t mc = warp_sum(b.mn[j] == m ? b.mc[j] : 0u);
+    if (lane == 0) { red[warp][j] = c; red[warp][NP + j] = m; red[warp][2 * NP + j] = mc; }
+    if (MASS) {
+      uint32_t q[12];
+      fx_split(b.ms[j], q);
+#pragma unroll
+      for (int i = 0; i < 12; ++i) {
+        const uint32_t sum = warp_sum(q[i]);
+        if (lane == 0) red[warp][3 * NP + 12 * j + i] = sum;
+      }
+    }
+  }
+}
+
+// Block stage, executed by warp 0 only: totals of all warp partials (every lane of warp 0 gets them).
+template <int NP, bool MASS>
+__device__ __forceinline__ void bk_warp0_totals(Buckets<NP, MASS> &b, uint32_t (*red)[48]) {
+  const int lane = threadIdx.x & 31;
+  const bool act = lane < kWarps;
+#pragma unroll
+  for (int j = 0; j < NP; ++j) {
+    b.cnt[j] = warp_sum(act ? red[lane][j] : 0u);
+    const uint32_t mv = act ? red[lane][NP + j] : 0xffffffffu;
+    const uint32_t m = warp_min(mv);
+    b.mn[j] = m;
+    b.mc[j] = warp_sum((act && mv == m) ? red[lane][2 * NP + j] : 0u);
+    if (MASS) {
+      uint32_t q[12];
+#pragma unroll
+      for (int i = 0; i < 12; ++i) q[i] = warp_sum(act ? red[lane][3 * NP + 12 * j + i] : 0u);
+      b.ms[j] = fx_join(q);
+    }
+  }
+}
+
 // Top-k boundary search over order keys.  Restates _search_topk (pivot_search.py:93-126): NP pivots
-// per pass at (j+1)/(NP+1) of [l, r], stop at the first pivot with N >= k and N - n_dup < k
+// per pass at (j+1)/(NP+1) of [l, r], stop at a pivot with N >= k and N - n_dup < k
 // (pivot_search.py:113-116).  Keys are integers, so the range always closes in <= 16 quaternary
 // passes — there is no range_eps collapse and no midpoint fallback.  Invariant: cnt(l) >= k > cnt(r).
+// Per pass: every warp scans its elements (only keys in (piv[0], r] can move a decision), one
+// barrier, warp 0 totals the partials and decides, a second barrier broadcasts the new range.
 template <int NP, class Src>
 __device__ KRes search_k(const Src &src, uint32_t l, uint32_t r, uint32_t cl, uint32_t cr, uint32_t k,
-                         TailSmem &sm) {
-  int iters = 0;
+                         Red &R) {
+  SearchState &st = R.sm.st;
+  if (threadIdx.x == 0) {
+    st.l = l; st.r = r; st.cl = cl; st.cr = cr; st.done = 0u; st.iters = 0;
+  }
+  __syncthreads();
   const Fx zero = fx_zero();
-  while (r - l > 1u) {
+  for (;;) {
+    l = st.l; r = st.r; cr = st.cr;
+    if (st.done || r - l <= 1u) break;
     uint32_t piv[NP];
     make_pivots<NP>(l, r, piv);
     Buckets<NP, false> b;
@@ -406,34 +504,42 @@ __device__ KRes search_k(const Src &src, uint32_t l, uint32_t r, uint32_t cl, ui
     for (int i = threadIdx.x; i < src.n; i += kThreads) {
       uint32_t bits, ix;
       src.get(i, bits, ix);
-      bk_add(b, piv, key_of_bits(bits), zero);
+      const uint32_t key = key_of_bits(bits);
+      if (key > piv[0] && key <= r) bk_add(b, piv, key, zero);
     }
-    bk_reduce(b, sm);
-    ++iters;
-    uint32_t cnt[NP], mn[NP], mc[NP];
-    {
-      uint32_t c = 0u, m = 0xffffffffu, x = 0u;
+    uint32_t(*red)[48] = R.sm.red[R.par];
+    R.par ^= 1;
+    bk_warp_partials(b, red);
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      bk_warp0_totals(b, red);
+      uint32_t cnt[NP], mn[NP], mc[NP];
+      uint32_t c = cr, m = 0xffffffffu, x = 0u;
 #pragma unroll
       for (int j = NP - 1; j >= 0; --j) {
-        c += sm.res_u[j];
-        if (sm.res_u[j] > 0u) { m = sm.res_u[NP + j]; x = sm.res_u[2 * NP + j]; }
+        c += b.cnt[j];
+        if (b.cnt[j] > 0u) { m = b.mn[j]; x = b.mc[j]; }
         cnt[j] = c; mn[j] = m; mc[j] = x;
       }
+      int J = -1;  // largest pivot still holding >= k keys above it
+#pragma unroll
+      for (int j = 0; j < NP; ++j) J = (cnt[j] >= k) ? j : J;
+      if (threadIdx.x == 0) {
+        st.iters += 1;
+        if (J >= 0 && cnt[J] - mc[J] < k) {
+          st.done = 1u; st.K = mn[J]; st.n_gt = cnt[J] - mc[J]; st.n_eq = mc[J];
+        } else {
+          if (J >= 0) { st.l = piv[J]; st.cl = cnt[J]; }
+          if (J + 1 < NP) { st.r = piv[J + 1]; st.cr = cnt[J + 1]; }
+        }
+      }
     }
-    __syncthreads();  // res_u is rewritten by the next pass
-#pragma unroll
-    for (int j = 0; j < NP; ++j)
-      if (cnt[j] >= k && cnt[j] - mc[j] < k) return KRes{mn[j], cnt[j] - mc[j], mc[j], iters};
-    uint32_t nl = l, ncl = cl, nr = r, ncr = cr;
-#pragma unroll
-    for (int j = 0; j < NP; ++j)
-      if (cnt[j] >= k) { nl = piv[j]; ncl = cnt[j]; }
-#pragma unroll
-    for (int j = NP - 1; j >= 0; --j)
-      if (cnt[j] < k) { nr = piv[j]; ncr = cnt[j]; }
-    l = nl; cl = ncl; r = nr; cr = ncr;
+    __syncthreads();
   }
-  return KRes{r, cr, cl - cr, iters};
+  const KRes res = st.done ? KRes{st.K, st.n_gt, st.n_eq, st.iters}
+                           : KRes{st.r, st.cr, st.cl - st.cr, st.iters};
+  __syncthreads();
+  return res;
 }
 
 struct PRes {
@@ -449,9 +555,16 @@ struct PRes {
 // pivot_search.py:177-191) is found directly, no resolve walk.  Invariant: M(l) >= T > M(r).
 template <int NP, class Src, class InS, class PiOf, class PiKey>
 __device__ PRes search_p(const Src &src, uint32_t l, uint32_t r, uint32_t cl, uint32_t cr, Fx Ml, Fx Mr,
-                         const Fx &T, InS in_s, PiOf pi_of, PiKey pi_key, TailSmem &sm) {
-  int iters = 0;
-  while (r - l > 1u) {
+                         const Fx &T, InS in_s, PiOf pi_of, PiKey pi_key, Red &R) {
+  SearchState &st = R.sm.st;
+  if (threadIdx.x == 0) {
+    st.l = l; st.r = r; st.cl = cl; st.cr = cr; st.Ml = Ml; st.Mr = Mr; st.done = 0u; st.iters = 0;
+  }
+  __syncthreads();
+  for (;;) {
+    l = st.l; r = st.r; cr = st.cr;
+    if (st.done || r - l <= 1u) break;
+    Mr = st.Mr;
     uint32_t piv[NP];
     make_pivots<NP>(l, r, piv);
     Buckets<NP, true> b;
@@ -460,42 +573,58 @@ __device__ PRes search_p(const Src &src, uint32_t l, uint32_t r, uint32_t cl, ui
       uint32_t bits, ix;
       src.get(i, bits, ix);
       const uint32_t key = key_of_bits(bits);
-      if (key > piv[0] && in_s(key, ix)) bk_add(b, piv, key, fx_from_double(pi_of(bits, i)));
+      if (key > piv[0] && key <= r && in_s(key, ix)) bk_add(b, piv, key, fx_from_double(pi_of(bits, i)));
     }
-    bk_reduce(b, sm);
-    ++iters;
-    uint32_t cnt[NP], mn[NP], mc[NP];
-    Fx M[NP];
-    {
-      uint32_t c = 0u, m = 0xffffffffu, x = 0u;
-      Fx s = fx_zero();
+    uint32_t(*red)[48] = R.sm.red[R.par];
+    R.par ^= 1;
+    bk_warp_partials(b, red);
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      bk_warp0_totals(b, red);
+      uint32_t cnt[NP], mn[NP], mc[NP];
+      Fx M[NP];
+      uint32_t c = cr, m = 0xffffffffu, x = 0u;
+      Fx sacc = Mr;
 #pragma unroll
       for (int j = NP - 1; j >= 0; --j) {
-        c += sm.res_u[j];
-        if (sm.res_u[j] > 0u) { m = sm.res_u[NP + j]; x = sm.res_u[2 * NP + j]; }
-        s = fx_add(s, fx_join(&sm.res_u[3 * NP + 12 * j]));
-        cnt[j] = c; mn[j] = m; mc[j] = x; M[j] = s;
+        c += b.cnt[j];
+        if (b.cnt[j] > 0u) { m = b.mn[j]; x = b.mc[j]; }
+        sacc = fx_add(sacc, b.ms[j]);
+        cnt[j] = c; mn[j] = m; mc[j] = x; M[j] = sacc;
+      }
+      int J = -1;  // largest pivot whose mass above still reaches p
+#pragma unroll
+      for (int j = 0; j < NP; ++j) J = fx_ge(M[j], T) ? j : J;
+      bool done = false;
+      Fx HJ = fx_zero();
+      uint32_t KJ = 0u, gJ = 0u, eJ = 0u, lJ = 0u, clJ = 0u, rJ = 0u, crJ = 0u;
+      Fx MlJ = fx_zero(), MrJ = fx_zero();
+#pragma unroll
+      for (int j = 0; j < NP; ++j) {
+        if (j == J) {
+          HJ = fx_sub(M[j], fx_mul_u32(fx_from_double(pi_key(mn[j])), mc[j]));
+          done = !fx_ge(HJ, T);
+          KJ = mn[j]; gJ = cnt[j] - mc[j]; eJ = mc[j];
+          lJ = piv[j]; clJ = cnt[j]; MlJ = M[j];
+        }
+        if (j == J + 1) { rJ = piv[j]; crJ = cnt[j]; MrJ = M[j]; }
+      }
+      if (threadIdx.x == 0) {
+        st.iters += 1;
+        if (done) {
+          st.done = 1u; st.K = KJ; st.n_gt = gJ; st.n_eq = eJ; st.H = HJ;
+        } else {
+          if (J >= 0) { st.l = lJ; st.cl = clJ; st.Ml = MlJ; }
+          if (J + 1 < NP) { st.r = rJ; st.cr = crJ; st.Mr = MrJ; }
+        }
       }
     }
     __syncthreads();
-#pragma unroll
-    for (int j = 0; j < NP; ++j) {
-      if (cnt[j] > 0u && fx_ge(M[j], T)) {
-        const Fx Hj = fx_sub(M[j], fx_mul_u32(fx_from_double(pi_key(mn[j])), mc[j]));
-        if (!fx_ge(Hj, T)) return PRes{mn[j], cnt[j] - mc[j], mc[j], Hj, iters};
-      }
-    }
-    uint32_t nl = l, ncl = cl, nr = r, ncr = cr;
-    Fx nMl = Ml, nMr = Mr;
-#pragma unroll
-    for (int j = 0; j < NP; ++j)
-      if (fx_ge(M[j], T)) { nl = piv[j]; ncl = cnt[j]; nMl = M[j]; }
-#pragma unroll
-    for (int j = NP - 1; j >= 0; --j)
-      if (!fx_ge(M[j], T)) { nr = piv[j]; ncr = cnt[j]; nMr = M[j]; }
-    l = nl; cl = ncl; r = nr; cr = ncr; Ml = nMl; Mr = nMr;
   }
-  return PRes{r, cr, cl - cr, Mr, iters};
+  const PRes res = st.done ? PRes{st.K, st.n_gt, st.n_eq, st.H, st.iters}
+                           : PRes{st.r, st.cr, st.cl - st.cr, st.Mr, st.iters};
+  __syncthreads();
+  return res;
 }
 
 __device__ __forceinline__ int nth_set_bit(uint32_t m, uint32_t n) {  // n >= 1
@@ -508,7 +637,8 @@ __device__ __forceinline__ int nth_set_bit(uint32_t m, uint32_t n) {  // n >= 1
 // This is the duplicate-trimming rule of _apply_plan (pipeline.py:53-56): occurrences beyond n_keep,
 // counted left to right, are dropped.
 template <class Src>
-__device__ uint32_t select_nth_eq(const Src &src, uint32_t K, uint32_t c, TailSmem &sm) {
+__device__ uint32_t select_nth_eq(const Src &src, uint32_t K, uint32_t c, Red &R) {
+  TailSmem &sm = R.sm;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int n = src.n;
   const int seg = ((n + kWarps - 1) / kWarps + 31) & ~31;
@@ -524,14 +654,14 @@ __device__ uint32_t select_nth_eq(const Src &src, uint32_t K, uint32_t c, TailSm
     }
     cnt += __popc(__ballot_sync(0xffffffffu, m));
   }
-  if (lane == 0) sm.red_u[warp][0] = cnt;
+  if (lane == 0) sm.sel[warp] = cnt;
   __syncthreads();
   if (threadIdx.x == 0) {
     uint32_t acc = 0u;
     int w = 0;
     for (; w < kWarps; ++w) {
-      if (acc + sm.red_u[w][0] >= c) break;
-      acc += sm.red_u[w][0];
+      if (acc + sm.sel[w] >= c) break;
+      acc += sm.sel[w];
     }
     sm.u[0] = (uint32_t)w;
     sm.u[1] = c - acc;
@@ -571,7 +701,7 @@ __device__ __forceinline__ bool kept_by(uint32_t key, uint32_t idx, uint32_t K, 
 
 // Exact block-wide sum of fx(v) over the elements accepted by fn(bits, idx, i, v); also counts them.
 template <class Src, class Fn>
-__device__ Fx block_mass(const Src &src, Fn fn, uint32_t &count, TailSmem &sm) {
+__device__ Fx block_mass(const Src &src, Fn fn, uint32_t &count, Red &R) {
   Buckets<1, true> b;
   b.cnt[0] = 0u; b.mn[0] = 0u; b.mc[0] = 0u; b.ms[0] = fx_zero();
   for (int i = threadIdx.x; i < src.n; i += kThreads) {
@@ -580,11 +710,9 @@ __device__ Fx block_mass(const Src &src, Fn fn, uint32_t &count, TailSmem &sm) {
     double v;
     if (fn(bits, ix, i, v)) { b.ms[0] = fx_add(b.ms[0], fx_from_double(v)); b.cnt[0] += 1u; }
   }
-  bk_reduce(b, sm);
-  count = sm.res_u[0];
-  const Fx r = fx_join(&sm.res_u[3]);
-  __syncthreads();
-  return r;
+  bk_reduce(b, R);
+  count = b.cnt[0];
+  return b.ms[0];
 }
 
 // Full-row output pass.  how: 0 = kept values only (background already -inf), 1 = every element,
@@ -601,8 +729,14 @@ __device__ void write_row(const T *in, T *out, int V, uint32_t K, uint32_t cut, 
 }
 
 template <typename T, int NP>
-__device__ __noinline__ void row_tail(const Params &P, int row, uint8_t *dsmem, TailSmem &sm) {
-  const int tid = threadIdx.x;
+__global__ void __launch_bounds__(kThreads) qrita_tail(Params P) {
+  extern __shared__ __align__(16) uint8_t dsmem[];
+  __shared__ TailSmem sm;
+  __shared__ uint32_t s_off[kMaxTailChunks + 1];
+  __shared__ uint32_t s_part[2][kWarps][5];
+  pdl_wait();  // outliers and chunk statistics of qrita_stream (and plans of qrita_prep)
+  const int row = blockIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int V = P.V;
   const int nch = P.nchunks;
   const RowPlan pl = P.plans[row];
@@ -618,31 +752,57 @@ __device__ __noinline__ void row_tail(const Params &P, int row, uint8_t *dsmem, 
   uint32_t *si = sb + kCapS;             // [kCapS] survivor indices
   double *sp = (double *)(si + kCapS);   // [kCapS] survivor exp / probability
 
-  // ---- per-row totals from the chunk statistics
-  if (tid == 0) {
-    uint32_t mx = 0u, cnt = 0u, nf = 0xffffffffu, ovf = 0u;
-    for (int c = 0; c < nch; ++c) {
-      const uint4 q = __ldcg(reinterpret_cast<const uint4 *>(P.cstats + (size_t)row * nch + c));
-      mx = max(mx, q.x);
-      cnt += q.y;
-      nf = min(nf, q.z);
-      ovf |= (q.y > (uint32_t)kCapChunk) ? 1u : 0u;
+  // ---- per-row totals and per-chunk outlier offsets (block scan over the chunk statistics)
+  uint32_t maxkey = 0u, minkey = 0xffffffffu, n_c = 0u, nf_col = 0xffffffffu, ovf = 0u;
+  for (int t0 = 0, par = 0; t0 < nch; t0 += kThreads, par ^= 1) {
+    const int c = t0 + tid;
+    uint4 q = make_uint4(0u, 0u, 0xffffffffu, 0xffffffffu);
+    if (c < nch) q = __ldcg(reinterpret_cast<const uint4 *>(P.cstats + (size_t)row * nch + c));
+    const uint32_t cc = q.y;
+    uint32_t incl = cc;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += v;
     }
-    sm.u[0] = mx; sm.u[1] = cnt; sm.u[2] = nf; sm.u[3] = ovf;
+    if (lane == 31) s_part[par][warp][0] = incl;
+    const uint32_t wmx = warp_max(c < nch ? q.x : 0u), wmn = warp_min(q.w), wnf = warp_min(q.z);
+    const uint32_t wov = warp_max(cc > (uint32_t)kCapChunk ? 1u : 0u);
+    if (lane == 0) { s_part[par][warp][1] = wmx; s_part[par][warp][2] = wmn; s_part[par][warp][3] = wnf;
+                     s_part[par][warp][4] = wov; }
+    __syncthreads();
+    uint32_t before = 0u, tile = 0u;
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) {
+      const uint32_t tw = s_part[par][w][0];
+      before += (w < warp) ? tw : 0u;
+      tile += tw;
+      maxkey = max(maxkey, s_part[par][w][1]);
+      minkey = min(minkey, s_part[par][w][2]);
+      nf_col = min(nf_col, s_part[par][w][3]);
+      ovf |= s_part[par][w][4];
+    }
+    if (c < nch && c < kMaxTailChunks) s_off[c] = n_c + before + incl - cc;
+    n_c += tile;
   }
-  __syncthreads();
-  const uint32_t maxkey = sm.u[0];
-  const uint32_t n_c = sm.u[1];
-  const uint32_t nf_col = sm.u[2];
-  const bool overflow = sm.u[3] != 0u;
+  if (tid == 0 && nch <= kMaxTailChunks) s_off[nch] = n_c;
+  const bool overflow = ovf != 0u || nch > kMaxTailChunks;
+  const uint32_t lo_row = minkey ? minkey - 1u : 0u;  // below every key of the row
   __syncthreads();
 
   qrita_row_metrics met;
   memset(&met, 0, sizeof(met));
   if (nf_col != 0xffffffffu) {  // validate_batch (core.py:124-128): reported, row left undefined
+    uint32_t first = 0xffffffffu;  // exact first non-finite column (error path only)
+    for (int i = (int)nf_col + tid; i < V; i += kThreads)
+      if (bits_nonfinite(Elem<T>::bits(in[i]))) { first = (uint32_t)i; break; }
+    first = warp_min(first);
+    if (lane == 0) sm.sel[warp] = first;
+    __syncthreads();
     if (tid == 0) {
+      for (int w = 0; w < kWarps; ++w) first = min(first, sm.sel[w]);
       P.status[row] |= ST_NONFINITE;
-      P.nf_col[row] = (int32_t)nf_col;
+      P.nf_col[row] = (int32_t)first;
     }
     return;
   }
@@ -664,20 +824,19 @@ __device__ __noinline__ void row_tail(const Params &P, int row, uint8_t *dsmem, 
   // ---- stage the outliers in shared memory (index order) when they fit
   const bool x_fits = sigma && !overflow && n_c <= (uint32_t)kCapX;
   if (x_fits) {
-    uint32_t base = 0u;
-    for (int c = 0; c < nch; ++c) {
-      const uint32_t cc = __ldcg(&P.cstats[(size_t)row * nch + c].count);
+    for (int c = warp; c < nch; c += kWarps) {  // one warp per chunk: coalesced slot reads
+      const uint32_t off = s_off[c], cc = s_off[c + 1] - off;
       const size_t slot = ((size_t)row * nch + c) * kCapChunk;
-      for (uint32_t j = tid; j < cc; j += kThreads) {
-        xb[base + j] = __ldcg(P.cand_bits + slot + j);
-        xi[base + j] = __ldcg(P.cand_idx + slot + j);
+      for (uint32_t j = lane; j < cc; j += 32) {
+        xb[off + j] = __ldcg(P.cand_bits + slot + j);
+        xi[off + j] = __ldcg(P.cand_idx + slot + j);
       }
-      base += cc;
     }
     __syncthreads();
   }
   const SrcX X{xb, xi, (int)n_c};
-  const SrcRow<T> R{in, V};
+  const SrcRow<T> RW{in, V};
+  Red red(sm);
 
   uint32_t Kf = 0u, cutf = kNoCut, kept = (uint32_t)V;
   bool k_used_x = false;  // the final kept set is a subset of X
@@ -693,9 +852,9 @@ __device__ __noinline__ void row_tail(const Params &P, int row, uint8_t *dsmem, 
     k_used_x = met.trunc_hit && x_fits;
     KRes kr;
     if (k_used_x) {
-      kr = search_k<NP>(X, pl.key_thr ? pl.key_thr - 1u : 0u, maxkey, n_c, 0u, k, sm);
+      kr = search_k<NP>(X, pl.key_thr ? pl.key_thr - 1u : 0u, maxkey, n_c, 0u, k, red);
     } else {
-      kr = search_k<NP>(R, 0u, maxkey, (uint32_t)V, 0u, k, sm);
+      kr = search_k<NP>(RW, lo_row, maxkey, (uint32_t)V, 0u, k, red);
       full_row = true;
     }
     met.k_search_iters = kr.iters;
@@ -703,7 +862,7 @@ __device__ __noinline__ void row_tail(const Params &P, int row, uint8_t *dsmem, 
     uint32_t ck = k - kr.n_gt;  // n_keep = n_dup - (N - k), pipeline.py:117
     if (nodup) ck = kr.n_eq;
     if (ck >= kr.n_eq) cutk = kNoCut;
-    else cutk = k_used_x ? select_nth_eq(X, Kk, ck, sm) : select_nth_eq(R, Kk, ck, sm);
+    else cutk = k_used_x ? select_nth_eq(X, Kk, ck, red) : select_nth_eq(RW, Kk, ck, red);
     n_s = kr.n_gt + ck;
     Kf = Kk; cutf = cutk; kept = n_s;
   }
@@ -735,7 +894,7 @@ __device__ __noinline__ void row_tail(const Params &P, int row, uint8_t *dsmem, 
       ns_cached = sm.u[4];
       __syncthreads();
       const SrcX S{sb, si, (int)ns_cached};
-      const Fx Dx = block_mass(S, [&](uint32_t, uint32_t, int i, double &v) { v = sp[i]; return true; }, cnt_dummy, sm);
+      const Fx Dx = block_mass(S, [&](uint32_t, uint32_t, int i, double &v) { v = sp[i]; return true; }, cnt_dummy, red);
       D = fx_to_double(Dx);
       for (int i = tid; i < (int)ns_cached; i += kThreads) sp[i] = sp[i] / D;
       __syncthreads();
@@ -743,12 +902,12 @@ __device__ __noinline__ void row_tail(const Params &P, int row, uint8_t *dsmem, 
     } else if (!topp_only && k_used_x) {
       const Fx Dx = block_mass(X, [&](uint32_t b, uint32_t ix, int, double &v) {
         if (!kept_by(key_of_bits(b), ix, Kk, cutk)) return false;
-        v = e_of(b); return true; }, cnt_dummy, sm);
+        v = e_of(b); return true; }, cnt_dummy, red);
       D = fx_to_double(Dx);
     } else {
-      const Fx Dx = block_mass(R, [&](uint32_t b, uint32_t ix, int, double &v) {
+      const Fx Dx = block_mass(RW, [&](uint32_t b, uint32_t ix, int, double &v) {
         if (!in_s(key_of_bits(b), ix)) return false;
-        v = e_of(b); return true; }, cnt_dummy, sm);
+        v = e_of(b); return true; }, cnt_dummy, red);
       D = fx_to_double(Dx);
       full_row = true;
     }
@@ -765,11 +924,11 @@ __device__ __noinline__ void row_tail(const Params &P, int row, uint8_t *dsmem, 
       Fx Mx = fx_zero();
       if (sigma) {
         if (x_fits) {
-          Mx = block_mass(X, [&](uint32_t b, uint32_t, int, double &v) { v = pi_bits(b); return true; }, cnt_dummy, sm);
+          Mx = block_mass(X, [&](uint32_t b, uint32_t, int, double &v) { v = pi_bits(b); return true; }, cnt_dummy, red);
         } else {
-          Mx = block_mass(R, [&](uint32_t b, uint32_t, int, double &v) {
+          Mx = block_mass(RW, [&](uint32_t b, uint32_t, int, double &v) {
             if (key_of_bits(b) < pl.key_thr) return false;
-            v = pi_bits(b); return true; }, cnt_dummy, sm);
+            v = pi_bits(b); return true; }, cnt_dummy, red);
         }
         met.outlier_prob_sum = fx_to_double(Mx);
         hit_ref = fx_ge(Mx, Tsp);
@@ -779,24 +938,24 @@ __device__ __noinline__ void row_tail(const Params &P, int row, uint8_t *dsmem, 
       if (met.trunc_hit && x_fits) {
         set_kind = 1; l0 = pl.key_thr ? pl.key_thr - 1u : 0u; cl0 = n_c; Ml0 = Mx;
       } else {
-        set_kind = 2; l0 = 0u; cl0 = (uint32_t)V;
-        Ml0 = block_mass(R, [&](uint32_t b, uint32_t, int, double &v) { v = pi_bits(b); return true; }, cnt_dummy, sm);
+        set_kind = 2; l0 = lo_row; cl0 = (uint32_t)V;
+        Ml0 = block_mass(RW, [&](uint32_t b, uint32_t, int, double &v) { v = pi_bits(b); return true; }, cnt_dummy, red);
         full_row = true;
       }
     } else if (s_cached) {
-      set_kind = 0; l0 = 0u; cl0 = ns_cached;
+      set_kind = 0; l0 = Kk - 1u; cl0 = ns_cached;  // every survivor has key >= Kk
       const SrcX S{sb, si, (int)ns_cached};
-      Ml0 = block_mass(S, [&](uint32_t, uint32_t, int i, double &v) { v = sp[i]; return true; }, cnt_dummy, sm);
+      Ml0 = block_mass(S, [&](uint32_t, uint32_t, int i, double &v) { v = sp[i]; return true; }, cnt_dummy, red);
     } else if (k_used_x) {
-      set_kind = 1; l0 = 0u; cl0 = n_s;
+      set_kind = 1; l0 = Kk - 1u; cl0 = n_s;
       Ml0 = block_mass(X, [&](uint32_t b, uint32_t ix, int, double &v) {
         if (!kept_by(key_of_bits(b), ix, Kk, cutk)) return false;
-        v = pi_bits(b); return true; }, cnt_dummy, sm);
+        v = pi_bits(b); return true; }, cnt_dummy, red);
     } else {
-      set_kind = 2; l0 = 0u; cl0 = n_s;
-      Ml0 = block_mass(R, [&](uint32_t b, uint32_t ix, int, double &v) {
+      set_kind = 2; l0 = Kk - 1u; cl0 = n_s;
+      Ml0 = block_mass(RW, [&](uint32_t b, uint32_t ix, int, double &v) {
         if (!in_s(key_of_bits(b), ix)) return false;
-        v = pi_bits(b); return true; }, cnt_dummy, sm);
+        v = pi_bits(b); return true; }, cnt_dummy, red);
     }
 
     if (!fx_ge(Ml0, Tsp)) {
@@ -809,13 +968,13 @@ __device__ __noinline__ void row_tail(const Params &P, int row, uint8_t *dsmem, 
         const SrcX S{sb, si, (int)ns_cached};
         pr = search_p<NP>(S, l0, maxkey, cl0, 0u, Ml0, zero, Tp,
                           [&](uint32_t, uint32_t) { return true; },
-                          [&](uint32_t, int i) { return sp[i]; }, pi_key, sm);
+                          [&](uint32_t, int i) { return sp[i]; }, pi_key, red);
       } else if (set_kind == 1) {
         pr = search_p<NP>(X, l0, maxkey, cl0, 0u, Ml0, zero, Tp, in_s,
-                          [&](uint32_t b, int) { return pi_bits(b); }, pi_key, sm);
+                          [&](uint32_t b, int) { return pi_bits(b); }, pi_key, red);
       } else {
-        pr = search_p<NP>(R, l0, maxkey, cl0, 0u, Ml0, zero, Tp, in_s,
-                          [&](uint32_t b, int) { return pi_bits(b); }, pi_key, sm);
+        pr = search_p<NP>(RW, l0, maxkey, cl0, 0u, Ml0, zero, Tp, in_s,
+                          [&](uint32_t b, int) { return pi_bits(b); }, pi_key, red);
       }
       met.p_search_iters = pr.iters;
       // smallest j with fsum(head + j * p_b) >= p (_min_dup_count, pivot_search.py:143-156), exactly
@@ -839,9 +998,9 @@ __device__ __noinline__ void row_tail(const Params &P, int row, uint8_t *dsmem, 
         // whole cluster (within S); if it is the top-k boundary cluster the top-k cut still applies
         cutf = (!topp_only && pr.K == Kk) ? cutk : kNoCut;
       } else if (set_kind == 2) {
-        cutf = select_nth_eq(R, pr.K, j, sm);
+        cutf = select_nth_eq(RW, pr.K, j, red);
       } else {
-        cutf = select_nth_eq(X, pr.K, j, sm);  // X is index-ordered and holds every copy of K
+        cutf = select_nth_eq(X, pr.K, j, red);  // X is index-ordered and holds every copy of K
       }
     }
   }
@@ -896,234 +1055,158 @@ template <> __device__ __forceinline__ uint4 neg_inf_vec<uint16_t>() {
   return make_uint4(0xff80ff80u, 0xff80ff80u, 0xff80ff80u, 0xff80ff80u);
 }
 
-struct MainSmem {
-  TailSmem tail;
-  uint32_t wcnt[8][kWarps];   // per (vector slot, warp) outlier counts
-  uint32_t woff[8][kWarps];   // their exclusive prefix in index order
-  uint32_t wmax[kWarps];
-  uint32_t wnf[kWarps];
-  int item;
-  int last;
-};
-
-// VEC: 16-byte aligned rows whose length is a multiple of the vector width.
-template <typename T, int NP, bool VEC>
-__global__ void __launch_bounds__(kThreads, 2) qrita_main(Params P) {
-  extern __shared__ __align__(16) uint8_t dsmem[];
-  __shared__ MainSmem ms;
+// One warp streams one 1024-element chunk: 128-bit loads (8 per lane for fp32, 4 for bf16), chunk
+// max / min / first non-finite column, order-stable outlier compaction with ballot/popc straight
+// into the chunk's HBM slots, and the output background (-inf for top-k rows, a copy for
+// passthrough rows).  No barriers: warps never wait for each other.
+template <typename T, bool VEC>
+__global__ void __launch_bounds__(kStreamThreads, 3) qrita_stream(Params P) {
   using VT = typename Vec<T>::type;
   constexpr int W = Vec<T>::W;
-  constexpr int U = kChunk / (kThreads * W);  // vectors per thread per chunk: 8 (f32) / 4 (bf16)
-  static_assert(U * kThreads * W == kChunk && U <= 8, "chunk shape");
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int U = kChunk / (32 * W);
+  static_assert(U * 32 * W == kChunk, "chunk shape");
+  pdl_launch_dependents();
+  const int lane = threadIdx.x & 31;
+  const int gwarp = (int)((blockIdx.x * kStreamThreads + threadIdx.x) >> 5);
+  const int nwarps = (int)((gridDim.x * kStreamThreads) >> 5);
   const int nch = P.nchunks;
   const bool inplace = (P.flags & QRITA_INPLACE) != 0;
+  const uint32_t lt = (1u << lane) - 1u;
+  bool waited = false;
 
-  for (;;) {
-    if (tid == 0) ms.item = (int)atomicAdd(P.work_ctr, 1u);
-    __syncthreads();
-    const int item = ms.item;
-    if (item >= P.total_items) break;
+  for (int item = gwarp; item < P.total_items; item += nwarps) {
     const int row = item / nch, c = item - row * nch;
-    const RowPlan *plp = P.plans + row;
-    const int mode = plp->mode;
-    const uint32_t key_thr = plp->key_thr;
-    const bool gather = plp->has_thr != 0;
-    // the stream writes the -inf background of top-k rows and copies passthrough rows; top-p-only
-    // rows are written once, by their tail
-    const bool write_bg = !inplace && (mode == MODE_TOPK || mode == MODE_TOPKP || mode == MODE_INVALID);
-    const bool write_copy = !inplace && mode == MODE_PASS;
-    const bool keep_l2 = (mode == MODE_TOPP) || inplace;  // the tail re-reads these rows
     const int c0 = c * kChunk;
     const int n = min(kChunk, P.V - c0);
     const T *src = (const T *)P.logits + (size_t)row * P.ld_in + c0;
     T *dst = (T *)P.out + (size_t)row * P.ld_out + c0;
-
-    uint32_t mx = 0u, nf = 0xffffffffu;
-    uint32_t myc[U];
     VT v[U];
     if (VEC) {
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        const int e = (u * kThreads + tid) * W;
-        if (e < n) v[u] = keep_l2 ? __ldg(reinterpret_cast<const VT *>(src + e))
-                                  : __ldcs(reinterpret_cast<const VT *>(src + e));
-      }
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int e = (u * kThreads + tid) * W;
-        uint32_t cnt = 0u;
-        if (e < n) {
-#pragma unroll
-          for (int w = 0; w < W; ++w) {
-            const uint32_t b = lane_bits<T>(v[u], w);
-            const uint32_t key = key_of_bits(b);
-            mx = max(mx, key);
-            if (bits_nonfinite(b)) nf = min(nf, (uint32_t)(c0 + e + w));
-            cnt += (gather && key >= key_thr) ? 1u : 0u;
-          }
-          if (write_bg) __stcs(reinterpret_cast<VT *>(dst + e), neg_inf_vec<T>());
-          else if (write_copy) __stcs(reinterpret_cast<VT *>(dst + e), v[u]);
-        }
-        myc[u] = cnt;
-      }
-    } else {
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        uint32_t cnt = 0u;
-#pragma unroll
-        for (int w = 0; w < W; ++w) {
-          const int e = (u * kThreads + tid) * W + w;
-          if (e < n) {
-            const T x = src[e];
-            const uint32_t b = Elem<T>::bits(x);
-            const uint32_t key = key_of_bits(b);
-            mx = max(mx, key);
-            if (bits_nonfinite(b)) nf = min(nf, (uint32_t)(c0 + e));
-            cnt += (gather && key >= key_thr) ? 1u : 0u;
-            if (write_bg) dst[e] = Elem<T>::neg_inf();
-            else if (write_copy) dst[e] = x;
-          }
-        }
-        myc[u] = cnt;
+        const int e = (u * 32 + lane) * W;
+        if (e + W <= n) v[u] = __ldcs(reinterpret_cast<const VT *>(src + e));
       }
     }
-    // ---- chunk reductions: max key, first non-finite column, outlier counts per (slot, warp)
-    mx = warp_max(mx);
-    nf = warp_min(nf);
-    if (lane == 0) { ms.wmax[warp] = mx; ms.wnf[warp] = nf; }
+    if (!waited) {  // the logits never depend on qrita_prep; the plans do
+      pdl_wait();
+      waited = true;
+    }
+    const RowPlan *plp = P.plans + row;
+    const int mode = plp->mode;
+    const uint32_t key_thr = plp->key_thr;
+    const bool gather = plp->has_thr != 0;
+    const bool write_bg = !inplace && (mode == MODE_TOPK || mode == MODE_TOPKP || mode == MODE_INVALID);
+    const bool write_copy = !inplace && mode == MODE_PASS;
+    const size_t slot = (size_t)item * kCapChunk;
+    uint32_t mx = 0u, mn = 0xffffffffu, nf = 0xffffffffu, base = 0u;
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      const uint32_t wc = warp_sum(myc[u]);
-      if (lane == 0) ms.wcnt[u][warp] = wc;
-    }
-    __syncthreads();
-    if (warp == 0) {
-      // exclusive scan over (slot, warp) in slot-major order == index order within the chunk
-      constexpr int NE = U * kWarps;
-      constexpr int PER = (NE + 31) / 32;
-      uint32_t vals[PER];
-      uint32_t s = 0u;
+      const int e = (u * 32 + lane) * W;
+      const bool full = VEC && (e + W <= n);
+      uint32_t b[W];
+      uint32_t mine = 0u, lower = 0u, tot = 0u;
 #pragma unroll
-      for (int q = 0; q < PER; ++q) {
-        const int e = lane * PER + q;
-        vals[q] = e < NE ? ms.wcnt[e / kWarps][e % kWarps] : 0u;
-        s += vals[q];
-      }
-      uint32_t incl = s;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += t;
-      }
-      uint32_t run = incl - s;
-#pragma unroll
-      for (int q = 0; q < PER; ++q) {
-        const int e = lane * PER + q;
-        if (e < NE) ms.woff[e / kWarps][e % kWarps] = run;
-        run += vals[q];
-      }
-      const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
-      const uint32_t cmax = warp_max(lane < kWarps ? ms.wmax[lane] : 0u);
-      const uint32_t cnf = warp_min(lane < kWarps ? ms.wnf[lane] : 0xffffffffu);
-      if (lane == 0) {
-        ChunkStat cs;
-        cs.maxkey = cmax; cs.count = total; cs.nf_col = cnf; cs.pad = 0u;
-        P.cstats[(size_t)row * nch + c] = cs;
-      }
-    }
-    __syncthreads();
-    // ---- outliers -> per-chunk HBM scratch, index order (order-stable compaction, gather_outliers)
-    // Within a (slot, warp) segment the index order is lane-major: element (lane, w) sits at
-    // 4*lane + w (8*lane + w for bf16), so its rank = outliers of lower lanes + my earlier w.
-    if (gather) {
-      const size_t slot = ((size_t)row * nch + c) * kCapChunk;
-      const uint32_t lt = (1u << lane) - 1u;
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int ebase = (u * kThreads + tid) * W;
-        uint32_t b[W];
-        uint32_t mine = 0u, lower = 0u;
-#pragma unroll
-        for (int w = 0; w < W; ++w) {
-          b[w] = 0u;
-          if (VEC) b[w] = lane_bits<T>(v[u], w);
-          else if (ebase + w < n) b[w] = Elem<T>::bits(src[ebase + w]);
-          const bool cand = (ebase + w < n) && key_of_bits(b[w]) >= key_thr;
-          mine |= cand ? (1u << w) : 0u;
-          lower += (uint32_t)__popc(__ballot_sync(0xffffffffu, cand) & lt);
+      for (int w = 0; w < W; ++w) {
+        const bool valid = e + w < n;
+        b[w] = full ? lane_bits<T>(v[u], w) : (valid ? Elem<T>::bits(src[e + w]) : 0u);
+        const uint32_t key = key_of_bits(b[w]);
+        if (valid) {
+          mx = max(mx, key);
+          mn = min(mn, key);
         }
-        uint32_t q = ms.woff[u][warp] + lower;
+        const bool cand = gather && valid && key >= key_thr;
+        const uint32_t bal = __ballot_sync(0xffffffffu, cand);
+        lower += (uint32_t)__popc(bal & lt);
+        tot += (uint32_t)__popc(bal);
+        mine |= cand ? (1u << w) : 0u;
+      }
+      // index order inside the warp chunk is (u, lane, w): my rank = earlier u + lower lanes + my w's
+      uint32_t q = base + lower;
 #pragma unroll
-        for (int w = 0; w < W; ++w) {
-          if ((mine >> w) & 1u) {
-            if (q < (uint32_t)kCapChunk) {
-              P.cand_bits[slot + q] = b[w];
-              P.cand_idx[slot + q] = (uint32_t)(c0 + ebase + w);
-            }
-            ++q;
+      for (int w = 0; w < W; ++w) {
+        if ((mine >> w) & 1u) {
+          if (q < (uint32_t)kCapChunk) {
+            P.cand_bits[slot + q] = b[w];
+            P.cand_idx[slot + q] = (uint32_t)(c0 + e + w);
           }
+          ++q;
+        }
+      }
+      base += tot;
+      if (write_bg || write_copy) {
+        if (full) {
+          __stcs(reinterpret_cast<VT *>(dst + e), write_bg ? neg_inf_vec<T>() : v[u]);
+        } else {
+#pragma unroll
+          for (int w = 0; w < W; ++w)
+            if (e + w < n) dst[e + w] = write_bg ? Elem<T>::neg_inf() : Elem<T>::from_bits(b[w]);
         }
       }
     }
-    // ---- completion: whoever finishes a row's last chunk runs the row tail
-    __threadfence();
-    __syncthreads();
-    if (tid == 0) {
-      const uint32_t t = atomicAdd(P.row_done + row, 1u);
-      ms.last = (t == (uint32_t)(nch - 1)) ? 1 : 0;
-    }
-    __syncthreads();
-    if (ms.last) {
-      __threadfence();
-      row_tail<T, NP>(P, row, dsmem, ms.tail);
-      __syncthreads();
-      if (tid == 0) P.row_done[row] = 0u;  // leave the workspace clean for the next call
-    }
-    __syncthreads();
-  }
-  // self-cleaning work counter
-  if (tid == 0) {
-    __threadfence();
-    const uint32_t t = atomicAdd(P.exit_ctr, 1u);
-    if (t == gridDim.x - 1) {
-      *P.work_ctr = 0u;
-      *P.exit_ctr = 0u;
-      __threadfence();
+    mx = warp_max(mx);
+    mn = warp_min(mn);
+    // +inf / +NaN sort above key(+inf), -inf / -NaN below key(-inf): no per-element test needed
+    nf = (mx >= 0xff800000u || mn <= 0x007fffffu) ? (uint32_t)c0 : 0xffffffffu;
+    if (lane == 0) {
+      ChunkStat cs;
+      cs.maxkey = mx; cs.count = base; cs.nf_col = nf; cs.minkey = mn;
+      P.cstats[item] = cs;
     }
   }
+  if (!waited) pdl_wait();
 }
 
-constexpr size_t kDynSmem = (size_t)kCapX * 8 + (size_t)kCapS * 16;
+constexpr size_t kTailDynSmem = (size_t)kCapX * 8 + (size_t)kCapS * 16;
 
 template <typename T, int NP, bool VEC>
-static cudaError_t launch_main(const Params &P, cudaStream_t st) {
-  auto kern = qrita_main<T, NP, VEC>;
-  static int grid_blocks = 0;  // per instantiation
-  if (grid_blocks == 0) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDynSmem);
+static cudaError_t launch_pipeline(const Params &P, cudaStream_t st, cudaEvent_t prep_done) {
+  static int stream_grid = 0;  // per instantiation
+  if (stream_grid == 0) {
+    cudaError_t e = cudaFuncSetAttribute(qrita_tail<T, NP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)kTailDynSmem);
     if (e != cudaSuccess) return e;
     int dev = 0, sms = 0, per_sm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, kDynSmem);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, qrita_stream<T, VEC>, kStreamThreads, 0);
     if (e != cudaSuccess) return e;
-    grid_blocks = sms * (per_sm < 1 ? 1 : per_sm);
+    stream_grid = sms * (per_sm < 1 ? 1 : per_sm);
   }
-  int grid = grid_blocks < P.total_items ? grid_blocks : P.total_items;
-  if (grid < 1) grid = 1;
-  kern<<<grid, kThreads, kDynSmem, st>>>(P);
-  return cudaGetLastError();
-}
-
-template <typename T>
-static cudaError_t launch_all(const Params &P, cudaStream_t st, bool vec) {
   qrita_prep<T><<<P.B, 256, 0, st>>>(P);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
+  if (prep_done) {
+    e = cudaEventRecord(prep_done, st);
+    if (e != cudaSuccess) return e;
+  }
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = prep_done ? 0 : 1;  // exact timing when profiled
+  cudaLaunchConfig_t cfg = {};
+  const int warps_needed = P.total_items;
+  int grid = (warps_needed + kStreamThreads / 32 - 1) / (kStreamThreads / 32);
+  if (grid > stream_grid) grid = stream_grid;
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3(kStreamThreads);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = st;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  e = cudaLaunchKernelEx(&cfg, qrita_stream<T, VEC>, P);
+  if (e != cudaSuccess) return e;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.gridDim = dim3((unsigned)P.B);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = kTailDynSmem;
+  return cudaLaunchKernelEx(&cfg, qrita_tail<T, NP>, P);
+}
+
+template <typename T>
+static cudaError_t launch_all(const Params &P, cudaStream_t st, bool vec, cudaEvent_t prep_done) {
   if (P.flags & QRITA_SEARCH_BINARY)
-    return vec ? launch_main<T, 1, true>(P, st) : launch_main<T, 1, false>(P, st);
-  return vec ? launch_main<T, 3, true>(P, st) : launch_main<T, 3, false>(P, st);
+    return vec ? launch_pipeline<T, 1, true>(P, st, prep_done) : launch_pipeline<T, 1, false>(P, st, prep_done);
+  return vec ? launch_pipeline<T, 3, true>(P, st, prep_done) : launch_pipeline<T, 3, false>(P, st, prep_done);
 }
 
 }  // namespace qrita

@@ -15,11 +15,12 @@ namespace qrita {
 // Constants
 // ------------------------------------------------------------------------------------------------
 constexpr int kTableSize = 200;  // tables.py:11
-constexpr int kChunk = 16384;    // elements per streaming work item
-constexpr int kCapChunk = 2048;  // outlier slots per chunk in the HBM scratch
+constexpr int kChunk = 1024;     // elements per streaming work item (one warp)
+constexpr int kCapChunk = 256;   // outlier slots per work item in the HBM scratch (25%)
 constexpr int kCapX = 8192;      // outliers staged in shared memory for the row tail
-constexpr int kCapS = 2048;      // top-k survivors whose probabilities are cached in shared memory
-constexpr int kMaxLeaves = 1024; // pairwise-sum leaves handled in parallel by qrita_prep
+constexpr int kCapS = 1024;      // top-k survivors whose probabilities are cached in shared memory
+constexpr int kStreamThreads = 256;
+constexpr int kMaxTailChunks = 2048;  // chunk offsets kept in shared memory by the row tail (V <= 2M)
 
 enum Mode : int32_t { MODE_INVALID = -1, MODE_PASS = 0, MODE_TOPK = 1, MODE_TOPP = 2, MODE_TOPKP = 3 };
 enum Status : int32_t { ST_BAD_K = 1, ST_BAD_P = 2, ST_NONFINITE = 4 };
@@ -43,7 +44,22 @@ struct ChunkStat {
   uint32_t maxkey;
   uint32_t count;     // outliers in the chunk (only the first kCapChunk are stored)
   uint32_t nf_col;    // first non-finite column, or 0xffffffff
-  uint32_t pad;
+  uint32_t minkey;
+};
+
+// numpy's pairwise-summation tree for the sigma sample (n = min(sample_size, V)), built on the host
+// once per call: leaves (<= 128 elements each) and internal nodes grouped by height, so the device
+// evaluates it level by level in parallel.  n_leaves == 0 means "too large, replay serially".
+constexpr int kPwMaxLeaves = 128;
+constexpr int kPwStage = 6144;  // samples staged in shared memory by qrita_prep
+struct PwTree {
+  int32_t n;
+  int16_t n_leaves, n_internal, n_levels, pad;
+  uint16_t leaf_off[kPwMaxLeaves];
+  uint16_t leaf_len[kPwMaxLeaves];
+  uint8_t left[kPwMaxLeaves];     // children (node ids: leaves 0.., internal nodes n_leaves..)
+  uint8_t right[kPwMaxLeaves];
+  uint8_t level_end[16];          // internal nodes [level_end[h-1], level_end[h]) have height h+1
 };
 
 struct Params {
@@ -61,19 +77,18 @@ struct Params {
   ChunkStat *cstats;
   uint32_t *cand_bits;
   uint32_t *cand_idx;
-  uint32_t *row_done;
-  uint32_t *work_ctr;
-  uint32_t *exit_ctr;
   int32_t *status;
   int32_t *nf_col;
   int nchunks;
   int total_items;
+  PwTree tree;
 };
 
-// Layout: [counters | status[B] | nf_col[B] | plans[B] | row_done[B] | chunk stats | outlier slots].
-// The status block only depends on B, so qrita_get_status needs no V.
+// Layout: [status[B] | nf_col[B] | plans[B] | chunk stats | outlier slots].  Every record is fully
+// rewritten by each call (no state carries over), and the status block only depends on B, so
+// qrita_get_status needs no V.
 struct WsLayout {
-  size_t ctrs, status, nf_col, plans, row_done, cstats, cand_bits, cand_idx, total;
+  size_t status, nf_col, plans, cstats, cand_bits, cand_idx, total;
 };
 
 inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
@@ -82,11 +97,9 @@ inline WsLayout ws_layout(int B, int V) {
   WsLayout L;
   const size_t nchunks = (size_t)((V + kChunk - 1) / kChunk);
   size_t off = 0;
-  L.ctrs = off;      off = align_up(off + 64, 256);
   L.status = off;    off = align_up(off + 4ull * (size_t)B, 256);
   L.nf_col = off;    off = align_up(off + 4ull * (size_t)B, 256);
   L.plans = off;     off = align_up(off + sizeof(RowPlan) * (size_t)B, 256);
-  L.row_done = off;  off = align_up(off + 4ull * (size_t)B, 256);
   L.cstats = off;    off = align_up(off + sizeof(ChunkStat) * (size_t)B * nchunks, 256);
   L.cand_bits = off; off = align_up(off + 4ull * (size_t)B * nchunks * kCapChunk, 256);
   L.cand_idx = off;  off = align_up(off + 4ull * (size_t)B * nchunks * kCapChunk, 256);
@@ -95,7 +108,7 @@ inline WsLayout ws_layout(int B, int V) {
 }
 
 
-cudaError_t launch_f32(const Params &P, cudaStream_t st, bool vec);
-cudaError_t launch_bf16(const Params &P, cudaStream_t st, bool vec);
+cudaError_t launch_f32(const Params &P, cudaStream_t st, bool vec, cudaEvent_t prep_done);
+cudaError_t launch_bf16(const Params &P, cudaStream_t st, bool vec, cudaEvent_t prep_done);
 
 }  // namespace qrita

@@ -28,27 +28,44 @@ def check(name, x, k, p, maxshow=4, **fl):
                     print("     row", x[i].tolist(), "want", keep.astype(int).tolist(), "got", got.astype(int).tolist())
     print(f"{name}: {nbad}/{x.shape[0]} bad")
 
-rng = np.random.default_rng(0)
-# 1. tiny top-p rows
-x = np.array([[2,1,0,0],[0,0,0,0],[9,0,0,0],[1,2,3,4]], np.float32)
-check("tiny-topp", x, [4]*4, [0.7,0.5,0.5,0.9])
-check("tiny-topk", x, [2]*4, [1.0]*4)
-check("tiny-comb", x, [3]*4, [0.9]*4)
-x = rng.normal(size=(16, 1000)).astype(np.float32)
-check("g1000-topp", x, [1000]*16, rng.uniform(0.1, 0.99, 16))
-check("g1000-topk", x, rng.integers(1, 1000, 16), [1.0]*16)
-check("g1000-comb", x, rng.integers(1, 1000, 16), rng.uniform(0.1, 0.99, 16))
-check("g1000-topp-nosigma", x, [1000]*16, rng.uniform(0.1, 0.99, 16), use_sigma_trunc=False)
-check("g1000-topk-nosigma", x, rng.integers(1, 1000, 16), [1.0]*16, use_sigma_trunc=False)
-x = rng.normal(size=(8, 40000)).astype(np.float32)
-check("g40000-topp", x, [40000]*8, rng.uniform(0.5, 0.99, 8))
-check("g40000-comb", x, rng.integers(1, 1024, 8), rng.uniform(0.5, 0.99, 8))
-check("g40000-comb-ff", x, rng.integers(1, 1024, 8), rng.uniform(0.5, 0.99, 8), force_fallback=True)
-xq = np.round(rng.normal(size=(8, 3000))*2).astype(np.float32)
-check("q3000-topk", xq, rng.integers(1, 3000, 8), [1.0]*8)
-check("q3000-topp", xq, [3000]*8, rng.uniform(0.1, 0.99, 8))
-# exhaustive-like for top-k V=5
-import itertools
-rows = np.array(list(itertools.product((0.,1.,2.), repeat=5)), np.float32)
-for kk in range(1, 6):
-    check(f"exh5-k{kk}", rows, [kk]*len(rows), [1.0]*len(rows), maxshow=2)
+if len(sys.argv) > 1 and sys.argv[1] == "stats":
+    pass
+else:
+  rng = np.random.default_rng(0)
+  # 1. tiny top-p rows
+  x = np.array([[2,1,0,0],[0,0,0,0],[9,0,0,0],[1,2,3,4]], np.float32)
+  check("tiny-topp", x, [4]*4, [0.7,0.5,0.5,0.9])
+  check("tiny-topk", x, [2]*4, [1.0]*4)
+  check("tiny-comb", x, [3]*4, [0.9]*4)
+  x = rng.normal(size=(16, 1000)).astype(np.float32)
+  check("g1000-topp", x, [1000]*16, rng.uniform(0.1, 0.99, 16))
+  check("g1000-topk", x, rng.integers(1, 1000, 16), [1.0]*16)
+  check("g1000-comb", x, rng.integers(1, 1000, 16), rng.uniform(0.1, 0.99, 16))
+  check("g1000-topp-nosigma", x, [1000]*16, rng.uniform(0.1, 0.99, 16), use_sigma_trunc=False)
+  check("g1000-topk-nosigma", x, rng.integers(1, 1000, 16), [1.0]*16, use_sigma_trunc=False)
+  x = rng.normal(size=(8, 40000)).astype(np.float32)
+  check("g40000-topp", x, [40000]*8, rng.uniform(0.5, 0.99, 8))
+  check("g40000-comb", x, rng.integers(1, 1024, 8), rng.uniform(0.5, 0.99, 8))
+  check("g40000-comb-ff", x, rng.integers(1, 1024, 8), rng.uniform(0.5, 0.99, 8), force_fallback=True)
+  xq = np.round(rng.normal(size=(8, 3000))*2).astype(np.float32)
+  check("q3000-topk", xq, rng.integers(1, 3000, 8), [1.0]*8)
+  check("q3000-topp", xq, [3000]*8, rng.uniform(0.1, 0.99, 8))
+  # exhaustive-like for top-k V=5
+  import itertools
+  rows = np.array(list(itertools.product((0.,1.,2.), repeat=5)), np.float32)
+  for kk in range(1, 6):
+      check(f"exh5-k{kk}", rows, [kk]*len(rows), [1.0]*len(rows), maxshow=2)
+
+if len(sys.argv) > 1 and sys.argv[1] == "stats":
+    import bench
+    for cfg in sys.argv[2:]:
+        x, k, p, dtype, desc = bench.workload(cfg)
+        tdt = torch.bfloat16 if dtype == "bf16" else torch.float32
+        xt = torch.from_numpy(x).cuda().to(tdt)
+        met = Q.ops.metrics_buffer(x.shape[0], xt.device)
+        Q.topk_topp(xt, torch.from_numpy(k).cuda(), torch.from_numpy(p).cuda(), metrics=met)
+        m = Q.ops.decode_metrics(met)
+        import statistics as st
+        for f in ("trunc_hit", "outlier_count", "k_search_iters", "p_search_iters", "kept_count", "full_row_path"):
+            vals = [r[f] for r in m]
+            print(f"{cfg} {f}: mean {st.mean(vals):.2f} max {max(vals)}")
