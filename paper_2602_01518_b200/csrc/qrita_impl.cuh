@@ -310,7 +310,8 @@ __global__ void __launch_bounds__(256) qrita_prep(Params P) {
 struct SearchState {
   uint32_t l, r, cl, cr;
   uint32_t done, K, n_gt, n_eq;
-  int iters, pad;
+  int iters, compact;
+  uint32_t n_act, pad;
   Fx Ml, Mr, H;
 };
 
@@ -326,8 +327,22 @@ struct TailSmem {
 struct Red {
   TailSmem &sm;
   int par;
-  __device__ explicit Red(TailSmem &s) : sm(s), par(0) {}
+  uint32_t *act_key;  // active-set buffer of the pivot searches (keys)
+  double *act_pi;     // and, for the top-p search, their probabilities
+  int act_cap_k, act_cap_p;
+  __device__ explicit Red(TailSmem &s) : sm(s), par(0), act_key(nullptr), act_pi(nullptr),
+                                         act_cap_k(0), act_cap_p(0) {}
 };
+
+// Warp-aggregated slot reservation in a shared counter.
+__device__ __forceinline__ uint32_t warp_reserve(uint32_t *ctr, bool want) {
+  const uint32_t bal = __ballot_sync(0xffffffffu, want);
+  const int lane = threadIdx.x & 31;
+  uint32_t base = 0u;
+  if (lane == 0 && bal) base = atomicAdd(ctr, (uint32_t)__popc(bal));
+  base = __shfl_sync(0xffffffffu, base, 0);
+  return base + (uint32_t)__popc(bal & ((1u << lane) - 1u));
+}
 
 // Element sources: i -> (fp32 bits, index)
 struct SrcX {  // outliers staged in shared memory (index order)
@@ -490,21 +505,46 @@ __device__ KRes search_k(const Src &src, uint32_t l, uint32_t r, uint32_t cl, ui
                          Red &R) {
   SearchState &st = R.sm.st;
   if (threadIdx.x == 0) {
-    st.l = l; st.r = r; st.cl = cl; st.cr = cr; st.done = 0u; st.iters = 0;
+    st.l = l; st.r = r; st.cl = cl; st.cr = cr; st.done = 0u; st.iters = 0; st.compact = 0; st.n_act = 0u;
   }
   __syncthreads();
   const Fx zero = fx_zero();
+  bool act = false;  // searching the compacted active set instead of src
   for (;;) {
     l = st.l; r = st.r; cr = st.cr;
     if (st.done || r - l <= 1u) break;
+    if (st.compact && !act) {
+      // keep only the keys that can still matter: (l, r]  (order is irrelevant to counts)
+      for (int i0 = 0; i0 < src.n; i0 += kThreads) {
+        const int i = i0 + threadIdx.x;
+        uint32_t key = 0u;
+        if (i < src.n) {
+          uint32_t bits, ix;
+          src.get(i, bits, ix);
+          key = key_of_bits(bits);
+        }
+        const bool keep = i < src.n && key > l && key <= r;
+        const uint32_t pos = warp_reserve(&st.n_act, keep);
+        if (keep) R.act_key[pos] = key;
+      }
+      act = true;
+      __syncthreads();
+    }
+    const int n = act ? (int)st.n_act : src.n;
     uint32_t piv[NP];
     make_pivots<NP>(l, r, piv);
     Buckets<NP, false> b;
     bk_init(b);
-    for (int i = threadIdx.x; i < src.n; i += kThreads) {
-      uint32_t bits, ix;
-      src.get(i, bits, ix);
-      const uint32_t key = key_of_bits(bits);
+    for (int i = threadIdx.x; i < n; i += kThreads) {
+      uint32_t key;
+      if (act) {
+        key = R.act_key[i];
+      } else {
+        uint32_t bits, ix;
+        src.get(i, bits, ix);
+        key = key_of_bits(bits);
+      }
+      // only keys inside (piv[0], r] can move a decision; everything above r is the known cr
       if (key > piv[0] && key <= r) bk_add(b, piv, key, zero);
     }
     uint32_t(*red)[48] = R.sm.red[R.par];
@@ -531,6 +571,8 @@ __device__ KRes search_k(const Src &src, uint32_t l, uint32_t r, uint32_t cl, ui
         } else {
           if (J >= 0) { st.l = piv[J]; st.cl = cnt[J]; }
           if (J + 1 < NP) { st.r = piv[J + 1]; st.cr = cnt[J + 1]; }
+          const uint32_t n_in = st.cl - st.cr;
+          if (!act && (int)n_in <= R.act_cap_k && 2 * (int)n_in <= n) st.compact = 1;
         }
       }
     }
@@ -559,21 +601,45 @@ __device__ PRes search_p(const Src &src, uint32_t l, uint32_t r, uint32_t cl, ui
   SearchState &st = R.sm.st;
   if (threadIdx.x == 0) {
     st.l = l; st.r = r; st.cl = cl; st.cr = cr; st.Ml = Ml; st.Mr = Mr; st.done = 0u; st.iters = 0;
+    st.compact = 0; st.n_act = 0u;
   }
   __syncthreads();
+  bool act = false;
   for (;;) {
     l = st.l; r = st.r; cr = st.cr;
     if (st.done || r - l <= 1u) break;
     Mr = st.Mr;
+    if (st.compact && !act) {
+      // survivors in (l, r] with their probabilities: later passes need neither src nor exp()
+      for (int i0 = 0; i0 < src.n; i0 += kThreads) {
+        const int i = i0 + threadIdx.x;
+        uint32_t key = 0u, bits = 0u, ix = 0u;
+        if (i < src.n) {
+          src.get(i, bits, ix);
+          key = key_of_bits(bits);
+        }
+        const bool keep = i < src.n && key > l && key <= r && in_s(key, ix);
+        const uint32_t pos = warp_reserve(&st.n_act, keep);
+        if (keep) { R.act_key[pos] = key; R.act_pi[pos] = pi_of(bits, i); }
+      }
+      act = true;
+      __syncthreads();
+    }
+    const int n = act ? (int)st.n_act : src.n;
     uint32_t piv[NP];
     make_pivots<NP>(l, r, piv);
     Buckets<NP, true> b;
     bk_init(b);
-    for (int i = threadIdx.x; i < src.n; i += kThreads) {
-      uint32_t bits, ix;
-      src.get(i, bits, ix);
-      const uint32_t key = key_of_bits(bits);
-      if (key > piv[0] && key <= r && in_s(key, ix)) bk_add(b, piv, key, fx_from_double(pi_of(bits, i)));
+    for (int i = threadIdx.x; i < n; i += kThreads) {
+      if (act) {
+        const uint32_t key = R.act_key[i];
+        if (key > piv[0] && key <= r) bk_add(b, piv, key, fx_from_double(R.act_pi[i]));
+      } else {
+        uint32_t bits, ix;
+        src.get(i, bits, ix);
+        const uint32_t key = key_of_bits(bits);
+        if (key > piv[0] && key <= r && in_s(key, ix)) bk_add(b, piv, key, fx_from_double(pi_of(bits, i)));
+      }
     }
     uint32_t(*red)[48] = R.sm.red[R.par];
     R.par ^= 1;
@@ -616,6 +682,8 @@ __device__ PRes search_p(const Src &src, uint32_t l, uint32_t r, uint32_t cl, ui
         } else {
           if (J >= 0) { st.l = lJ; st.cl = clJ; st.Ml = MlJ; }
           if (J + 1 < NP) { st.r = rJ; st.cr = crJ; st.Mr = MrJ; }
+          const uint32_t n_in = st.cl - st.cr;
+          if (!act && (int)n_in <= R.act_cap_p && 2 * (int)n_in <= n) st.compact = 1;
         }
       }
     }
@@ -751,6 +819,8 @@ __global__ void __launch_bounds__(kThreads) qrita_tail(Params P) {
   uint32_t *sb = xi + kCapX;             // [kCapS] survivor bits
   uint32_t *si = sb + kCapS;             // [kCapS] survivor indices
   double *sp = (double *)(si + kCapS);   // [kCapS] survivor exp / probability
+  double *ap = sp + kCapS;               // [kCapA] active-set probabilities (top-p search)
+  uint32_t *ak = (uint32_t *)(ap + kCapA);  // [kCapA] active-set keys (3*kCapA keys for top-k)
 
   // ---- per-row totals and per-chunk outlier offsets (block scan over the chunk statistics)
   uint32_t maxkey = 0u, minkey = 0xffffffffu, n_c = 0u, nf_col = 0xffffffffu, ovf = 0u;
@@ -837,6 +907,10 @@ __global__ void __launch_bounds__(kThreads) qrita_tail(Params P) {
   const SrcX X{xb, xi, (int)n_c};
   const SrcRow<T> RW{in, V};
   Red red(sm);
+  red.act_key = (uint32_t *)ap;  // the top-k search runs first: the whole region holds keys
+  red.act_pi = ap;
+  red.act_cap_k = 3 * kCapA;
+  red.act_cap_p = kCapA;
 
   uint32_t Kf = 0u, cutf = kNoCut, kept = (uint32_t)V;
   bool k_used_x = false;  // the final kept set is a subset of X
@@ -869,6 +943,7 @@ __global__ void __launch_bounds__(kThreads) qrita_tail(Params P) {
 
   // ================= top-p stage: pipeline.py:161-196 (p only) and :226-239 (k then p) ============
   if (mode == MODE_TOPP || mode == MODE_TOPKP) {
+    red.act_key = ak;  // (key, probability) pairs from here on
     const Fx Tp = pl.t_p, Tsp = pl.t_sp;
     const bool topp_only = (mode == MODE_TOPP);
     auto in_s = [&](uint32_t key, uint32_t idx) -> bool { return topp_only || kept_by(key, idx, Kk, cutk); };
@@ -1059,34 +1134,58 @@ template <> __device__ __forceinline__ uint4 neg_inf_vec<uint16_t>() {
 // max / min / first non-finite column, order-stable outlier compaction with ballot/popc straight
 // into the chunk's HBM slots, and the output background (-inf for top-k rows, a copy for
 // passthrough rows).  No barriers: warps never wait for each other.
+__device__ __forceinline__ float max_nan(float a, float b) {
+  float r;
+  asm("max.NaN.f32 %0, %1, %2;" : "=f"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ float min_nan(float a, float b) {
+  float r;
+  asm("min.NaN.f32 %0, %1, %2;" : "=f"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ bool f_nonfinite(float x) { return bits_nonfinite(__float_as_uint(x)); }
+
+template <typename T>
+__device__ __forceinline__ float lane_f(const typename Vec<T>::type &v, int w) {
+  return __uint_as_float(lane_bits<T>(v, w));
+}
+
+// One warp streams one 1024-element chunk: 128-bit loads (8 per lane for fp32, 4 for bf16), chunk
+// max / min with NaN-propagating min/max (non-finite values surface in the chunk extrema, no
+// per-element test), order-stable outlier compaction with ballot/popc staged in shared memory and
+// written out coalesced, and the output background (-inf for top-k rows, a copy for passthrough
+// rows).  No block barriers: warps never wait for each other.
 template <typename T, bool VEC>
 __global__ void __launch_bounds__(kStreamThreads, 3) qrita_stream(Params P) {
   using VT = typename Vec<T>::type;
   constexpr int W = Vec<T>::W;
   constexpr int U = kChunk / (32 * W);
+  constexpr int NWB = kStreamThreads / 32;
   static_assert(U * 32 * W == kChunk, "chunk shape");
+  __shared__ uint32_t s_cb[NWB][kCapChunk];
+  __shared__ uint32_t s_ci[NWB][kCapChunk];
   pdl_launch_dependents();
-  const int lane = threadIdx.x & 31;
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int gwarp = (int)((blockIdx.x * kStreamThreads + threadIdx.x) >> 5);
   const int nwarps = (int)((gridDim.x * kStreamThreads) >> 5);
   const int nch = P.nchunks;
   const bool inplace = (P.flags & QRITA_INPLACE) != 0;
   const uint32_t lt = (1u << lane) - 1u;
+  const float qnan = __uint_as_float(0x7fffffffu);
   bool waited = false;
 
   for (int item = gwarp; item < P.total_items; item += nwarps) {
     const int row = item / nch, c = item - row * nch;
     const int c0 = c * kChunk;
     const int n = min(kChunk, P.V - c0);
+    const bool whole = VEC && n == kChunk;  // warp-uniform fast path
     const T *src = (const T *)P.logits + (size_t)row * P.ld_in + c0;
     T *dst = (T *)P.out + (size_t)row * P.ld_out + c0;
     VT v[U];
-    if (VEC) {
+    if (whole) {
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int e = (u * 32 + lane) * W;
-        if (e + W <= n) v[u] = __ldcs(reinterpret_cast<const VT *>(src + e));
-      }
+      for (int u = 0; u < U; ++u) v[u] = __ldcs(reinterpret_cast<const VT *>(src + (u * 32 + lane) * W));
     }
     if (!waited) {  // the logits never depend on qrita_prep; the plans do
       pdl_wait();
@@ -1094,70 +1193,100 @@ __global__ void __launch_bounds__(kStreamThreads, 3) qrita_stream(Params P) {
     }
     const RowPlan *plp = P.plans + row;
     const int mode = plp->mode;
-    const uint32_t key_thr = plp->key_thr;
-    const bool gather = plp->has_thr != 0;
+    // outlier iff z >= thr (float compare: -0.0 == +0.0 as in the reference); NaN threshold = none
+    const float thr = plp->has_thr ? __uint_as_float(bits_of_key(plp->key_thr)) : qnan;
     const bool write_bg = !inplace && (mode == MODE_TOPK || mode == MODE_TOPKP || mode == MODE_INVALID);
     const bool write_copy = !inplace && mode == MODE_PASS;
-    const size_t slot = (size_t)item * kCapChunk;
-    uint32_t mx = 0u, mn = 0xffffffffu, nf = 0xffffffffu, base = 0u;
+    float fmx = __uint_as_float(0xff800000u), fmn = __uint_as_float(0x7f800000u);
+    uint32_t base = 0u;
+    if (whole) {
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int e = (u * 32 + lane) * W;
-      const bool full = VEC && (e + W <= n);
-      uint32_t b[W];
-      uint32_t mine = 0u, lower = 0u, tot = 0u;
+      for (int u = 0; u < U; ++u) {
+        const int e = (u * 32 + lane) * W;
+        uint32_t bal[W];
+        uint32_t any = 0u;
 #pragma unroll
-      for (int w = 0; w < W; ++w) {
-        const bool valid = e + w < n;
-        b[w] = full ? lane_bits<T>(v[u], w) : (valid ? Elem<T>::bits(src[e + w]) : 0u);
-        const uint32_t key = key_of_bits(b[w]);
-        if (valid) {
-          mx = max(mx, key);
-          mn = min(mn, key);
+        for (int w = 0; w < W; ++w) {
+          const float x = lane_f<T>(v[u], w);
+          fmx = max_nan(fmx, x);
+          fmn = min_nan(fmn, x);
+          bal[w] = __ballot_sync(0xffffffffu, x >= thr);
+          any |= bal[w];
         }
-        const bool cand = gather && valid && key >= key_thr;
-        const uint32_t bal = __ballot_sync(0xffffffffu, cand);
-        lower += (uint32_t)__popc(bal & lt);
-        tot += (uint32_t)__popc(bal);
-        mine |= cand ? (1u << w) : 0u;
-      }
-      // index order inside the warp chunk is (u, lane, w): my rank = earlier u + lower lanes + my w's
-      uint32_t q = base + lower;
+        if (any) {  // warp-uniform: stage this slot's outliers in index order (u, lane, w)
+          uint32_t q = base;
 #pragma unroll
-      for (int w = 0; w < W; ++w) {
-        if ((mine >> w) & 1u) {
-          if (q < (uint32_t)kCapChunk) {
-            P.cand_bits[slot + q] = b[w];
-            P.cand_idx[slot + q] = (uint32_t)(c0 + e + w);
+          for (int w = 0; w < W; ++w) q += (uint32_t)__popc(bal[w] & lt);
+#pragma unroll
+          for (int w = 0; w < W; ++w) {
+            if ((bal[w] >> lane) & 1u) {
+              if (q < (uint32_t)kCapChunk) {
+                s_cb[wib][q] = lane_bits<T>(v[u], w);
+                s_ci[wib][q] = (uint32_t)(c0 + e + w);
+              }
+              ++q;
+            }
           }
-          ++q;
-        }
-      }
-      base += tot;
-      if (write_bg || write_copy) {
-        if (full) {
-          __stcs(reinterpret_cast<VT *>(dst + e), write_bg ? neg_inf_vec<T>() : v[u]);
-        } else {
 #pragma unroll
-          for (int w = 0; w < W; ++w)
-            if (e + w < n) dst[e + w] = write_bg ? Elem<T>::neg_inf() : Elem<T>::from_bits(b[w]);
+          for (int w = 0; w < W; ++w) base += (uint32_t)__popc(bal[w]);
+        }
+        if (write_bg) __stcs(reinterpret_cast<VT *>(dst + e), neg_inf_vec<T>());
+        else if (write_copy) __stcs(reinterpret_cast<VT *>(dst + e), v[u]);
+      }
+    } else {
+      // ragged / unaligned chunk: element-wise, same (u, lane, w) order
+      for (int u = 0; u < U; ++u) {
+        const int e = (u * 32 + lane) * W;
+        uint32_t bal[W];
+        uint32_t b[W];
+#pragma unroll
+        for (int w = 0; w < W; ++w) {
+          const bool valid = e + w < n;
+          b[w] = valid ? Elem<T>::bits(src[e + w]) : 0u;
+          const float x = __uint_as_float(b[w]);
+          if (valid) {
+            fmx = max_nan(fmx, x);
+            fmn = min_nan(fmn, x);
+          }
+          bal[w] = __ballot_sync(0xffffffffu, valid && x >= thr);
+          if (valid && (write_bg || write_copy)) dst[e + w] = write_bg ? Elem<T>::neg_inf() : src[e + w];
+        }
+        uint32_t q = base;
+#pragma unroll
+        for (int w = 0; w < W; ++w) q += (uint32_t)__popc(bal[w] & lt);
+#pragma unroll
+        for (int w = 0; w < W; ++w) {
+          if ((bal[w] >> lane) & 1u) {
+            if (q < (uint32_t)kCapChunk) { s_cb[wib][q] = b[w]; s_ci[wib][q] = (uint32_t)(c0 + e + w); }
+            ++q;
+          }
+          base += (uint32_t)__popc(bal[w]);
         }
       }
     }
-    mx = warp_max(mx);
-    mn = warp_min(mn);
-    // +inf / +NaN sort above key(+inf), -inf / -NaN below key(-inf): no per-element test needed
-    nf = (mx >= 0xff800000u || mn <= 0x007fffffu) ? (uint32_t)c0 : 0xffffffffu;
+    // chunk statistics; NaN / inf anywhere shows up in the NaN-propagating extrema
+    const bool nf_lane = f_nonfinite(fmx) || f_nonfinite(fmn);
+    const uint32_t nf = __any_sync(0xffffffffu, nf_lane) ? (uint32_t)c0 : 0xffffffffu;
+    const uint32_t mx = warp_max(key_of_bits(__float_as_uint(fmx)));
+    const uint32_t mn = warp_min(key_of_bits(__float_as_uint(fmn)));
+    __syncwarp();
+    const size_t slot = (size_t)item * kCapChunk;
+    const uint32_t nst = base < (uint32_t)kCapChunk ? base : (uint32_t)kCapChunk;
+    for (uint32_t j = lane; j < nst; j += 32) {
+      P.cand_bits[slot + j] = s_cb[wib][j];
+      P.cand_idx[slot + j] = s_ci[wib][j];
+    }
     if (lane == 0) {
       ChunkStat cs;
       cs.maxkey = mx; cs.count = base; cs.nf_col = nf; cs.minkey = mn;
       P.cstats[item] = cs;
     }
+    __syncwarp();
   }
   if (!waited) pdl_wait();
 }
 
-constexpr size_t kTailDynSmem = (size_t)kCapX * 8 + (size_t)kCapS * 16;
+constexpr size_t kTailDynSmem = (size_t)kCapX * 8 + (size_t)kCapS * 16 + (size_t)kCapA * 12;
 
 template <typename T, int NP, bool VEC>
 static cudaError_t launch_pipeline(const Params &P, cudaStream_t st, cudaEvent_t prep_done) {

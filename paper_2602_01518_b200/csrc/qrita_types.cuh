@@ -19,6 +19,7 @@ constexpr int kChunk = 1024;     // elements per streaming work item (one warp)
 constexpr int kCapChunk = 256;   // outlier slots per work item in the HBM scratch (25%)
 constexpr int kCapX = 8192;      // outliers staged in shared memory for the row tail
 constexpr int kCapS = 1024;      // top-k survivors whose probabilities are cached in shared memory
+constexpr int kCapA = 1024;      // active set of the top-p pivot search (3x as many keys for top-k)
 constexpr int kStreamThreads = 256;
 constexpr int kMaxTailChunks = 2048;  // chunk offsets kept in shared memory by the row tail (V <= 2M)
 
