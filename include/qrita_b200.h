@@ -52,7 +52,8 @@ enum {
   QRITA_FORCE_FALLBACK  = 1 << 2, /* force_fallback=True: gather, but search the full row           */
   QRITA_NO_DUP          = 1 << 3, /* duplication_handling_enabled=False: keep whole boundary cluster*/
   QRITA_INPLACE         = 1 << 4, /* out == logits (pipeline.py:72-74)                               */
-  QRITA_RESERVED_5      = 1 << 5  /* reserved (rejected)                                            */
+  QRITA_RESERVED_5      = 1 << 5, /* reserved (rejected)                                            */
+  QRITA_DEBUG_TIMING    = 1 << 6  /* record per-row tail phase timestamps (qrita_get_timing)        */
 };
 
 /* return codes */
@@ -120,6 +121,10 @@ int qrita_topk_topp_ex(const void *logits, int64_t ld_in, int dtype, int B, int 
  * returns QRITA_OK or QRITA_EINVAL_K / QRITA_EINVAL_P / QRITA_ENONFINITE, and fills *row / *col
  * (col = first non-finite column, or -1). */
 int qrita_get_status(const void *workspace, int B, int *row, int *col, qrita_stream_t stream);
+
+/* Synchronises `stream` and copies the [B][16] tail phase timestamps (ns, %globaltimer) of the last
+ * QRITA_DEBUG_TIMING call on this workspace into host memory `out`. */
+int qrita_get_timing(const void *workspace, int B, unsigned long long *out, qrita_stream_t stream);
 
 const char *qrita_strerror(int code);
 

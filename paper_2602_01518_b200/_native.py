@@ -20,6 +20,7 @@ NO_SIGMA = 1 << 1
 FORCE_FALLBACK = 1 << 2
 NO_DUP = 1 << 3
 INPLACE = 1 << 4
+DEBUG_TIMING = 1 << 6
 
 OK = 0
 EINVAL_ARG = 1
@@ -32,7 +33,7 @@ ENCCL = 7
 
 EXPORTED_SYMBOLS = (
     "qrita_workspace_bytes", "qrita_workspace_init", "qrita_topk_topp", "qrita_topk_topp_ex",
-    "qrita_get_status",
+    "qrita_get_status", "qrita_get_timing",
     "qrita_strerror", "qrita_version",
 )
 
@@ -84,6 +85,8 @@ def load() -> ctypes.CDLL:
     lib.qrita_topk_topp_ex.restype = i32
     lib.qrita_get_status.argtypes = [vp, i32, ctypes.POINTER(i32), ctypes.POINTER(i32), vp]
     lib.qrita_get_status.restype = i32
+    lib.qrita_get_timing.argtypes = [vp, i32, vp, vp]
+    lib.qrita_get_timing.restype = i32
     lib.qrita_strerror.argtypes = [i32]
     lib.qrita_strerror.restype = ctypes.c_char_p
     lib.qrita_version.argtypes = []

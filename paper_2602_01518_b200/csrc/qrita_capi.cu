@@ -102,7 +102,8 @@ int qrita_topk_topp_ex(const void *logits, int64_t ld_in, int dtype, int B, int 
   if (!logits || !out || !k || !p || !workspace) return QRITA_EINVAL_ARG;
   if (B < 1 || V < 1 || ld_in < V || ld_out < V || sample_size < 1) return QRITA_EINVAL_ARG;
   if (dtype != QRITA_DTYPE_F32 && dtype != QRITA_DTYPE_BF16) return QRITA_EINVAL_ARG;
-  if (flags & ~(QRITA_SEARCH_BINARY | QRITA_NO_SIGMA | QRITA_FORCE_FALLBACK | QRITA_NO_DUP | QRITA_INPLACE))
+  if (flags & ~(QRITA_SEARCH_BINARY | QRITA_NO_SIGMA | QRITA_FORCE_FALLBACK | QRITA_NO_DUP | QRITA_INPLACE |
+                QRITA_DEBUG_TIMING))
     return QRITA_EINVAL_ARG;
   const bool inplace = (flags & QRITA_INPLACE) != 0;
   if (inplace != (logits == out)) return QRITA_EINVAL_ARG;
@@ -124,6 +125,7 @@ int qrita_topk_topp_ex(const void *logits, int64_t ld_in, int dtype, int B, int 
   P.cand_idx = (uint32_t *)(ws + L.cand_idx);
   P.status = (int32_t *)(ws + L.status);
   P.nf_col = (int32_t *)(ws + L.nf_col);
+  P.dbg = (unsigned long long *)(ws + L.dbg);
   P.nchunks = (int)nchunks;
   P.total_items = (int)((size_t)B * nchunks);
   pw_tree(sample_size < V ? sample_size : V, P.tree);
@@ -165,6 +167,14 @@ int qrita_get_status(const void *workspace, int B, int *row, int *col, qrita_str
   }
   free(st);
   return code;
+}
+
+int qrita_get_timing(const void *workspace, int B, unsigned long long *out, qrita_stream_t stream) {
+  if (!workspace || !out || B < 1) return QRITA_EINVAL_ARG;
+  if (cudaStreamSynchronize((cudaStream_t)stream) != cudaSuccess) return QRITA_ECUDA;
+  const WsLayout L = ws_layout(B, 1);
+  return cudaMemcpy(out, (const uint8_t *)workspace + L.dbg, 128ull * (size_t)B, cudaMemcpyDeviceToHost) ==
+                 cudaSuccess ? QRITA_OK : QRITA_ECUDA;
 }
 
 const char *qrita_strerror(int code) {

@@ -199,7 +199,21 @@ __global__ void __launch_bounds__(256) qrita_prep(Params P) {
     const int n = tr.n;
     const int nl = tr.n_leaves;
     if (nl > 0) {
-      for (int i = tid; i < n; i += blockDim.x) s_x[i] = __uint_as_float(Elem<T>::bits(a[i]));
+      // batch the loads: 8 independent loads in flight per thread instead of one load per trip
+      constexpr int R = 8;
+      for (int i0 = tid; i0 < n; i0 += 256 * R) {
+        float tmp[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const int i = i0 + r * 256;
+          tmp[r] = i < n ? __uint_as_float(Elem<T>::bits(__ldg(a + i))) : 0.0f;
+        }
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const int i = i0 + r * 256;
+          if (i < n) s_x[i] = tmp[r];
+        }
+      }
       __syncthreads();
       // numpy's 8-accumulator leaf loop, one thread per (leaf, accumulator)
       for (int q = tid; q < nl * 8; q += blockDim.x) {
@@ -319,8 +333,12 @@ struct TailSmem {
   uint32_t red[2][kWarps][48];  // double-buffered per-warp partials of the block reductions
   uint32_t sel[kWarps];         // per-warp counts of select_nth_eq
   uint32_t u[8];                // broadcast scalars
+  uint32_t ctot[kWarps];        // bracket pass: per-warp count totals
+  Fx mtot[kWarps];              // bracket pass: per-warp mass totals
   SearchState st;
 };
+
+constexpr int kBins = 256;  // buckets of the bracketing pass (== kThreads: one bucket per thread)
 
 // Block-reduction context.  `par` is block-uniform: consecutive reductions alternate between the
 // two partial buffers, so each reduction needs a single barrier.
@@ -330,8 +348,10 @@ struct Red {
   uint32_t *act_key;  // active-set buffer of the pivot searches (keys)
   double *act_pi;     // and, for the top-p search, their probabilities
   int act_cap_k, act_cap_p;
+  uint32_t *hcnt;              // [kBins] bracket-pass counts   (aliases the active-set region)
+  unsigned long long *hms;     // [5][kBins] bracket-pass masses as 32-bit pieces
   __device__ explicit Red(TailSmem &s) : sm(s), par(0), act_key(nullptr), act_pi(nullptr),
-                                         act_cap_k(0), act_cap_p(0) {}
+                                         act_cap_k(0), act_cap_p(0), hcnt(nullptr), hms(nullptr) {}
 };
 
 // Warp-aggregated slot reservation in a shared counter.
@@ -500,6 +520,136 @@ __device__ __forceinline__ void bk_warp0_totals(Buckets<NP, MASS> &b, uint32_t (
 // passes — there is no range_eps collapse and no midpoint fallback.  Invariant: cnt(l) >= k > cnt(r).
 // Per pass: every warp scans its elements (only keys in (piv[0], r] can move a decision), one
 // barrier, warp 0 totals the partials and decides, a second barrier broadcasts the new range.
+// Exact block-wide sum of fx(v) over the elements accepted by fn(bits, idx, i, v); also counts them.
+template <class Src, class Fn>
+__device__ Fx block_mass(const Src &src, Fn fn, uint32_t &count, Red &R) {
+  Buckets<1, true> b;
+  b.cnt[0] = 0u; b.mn[0] = 0u; b.mc[0] = 0u; b.ms[0] = fx_zero();
+  for (int i = threadIdx.x; i < src.n; i += kThreads) {
+    uint32_t bits, ix;
+    src.get(i, bits, ix);
+    double v;
+    if (fn(bits, ix, i, v)) { b.ms[0] = fx_add(b.ms[0], fx_from_double(v)); b.cnt[0] += 1u; }
+  }
+  bk_reduce(b, R);
+  count = b.cnt[0];
+  return b.ms[0];
+}
+
+// Bracketing pass: one pass with 255 pivots at power-of-two spacing (a 256-bucket histogram in
+// shared memory, one bucket per thread for the scan).  It narrows (l, r] to the bucket that holds
+// the k-th key (top-k) / the nucleus crossing (top-p) with exact counts and masses at both ends, so
+// the quaternary passes that follow start from a ~256x narrower range.  Bucket b covers keys
+// (l + b*2^s, l + (b+1)*2^s].  Returns true when the bucket is a single key (search finished).
+__device__ __forceinline__ int bracket_shift(uint32_t w) {  // smallest s with w <= 256 * 2^s
+  if (w <= (uint32_t)kBins) return 0;
+  const int lg = 32 - __clz(w - 1u);  // ceil(log2(w))
+  return lg - 8;
+}
+
+template <bool MASS, class KeyOf, class PiOf>
+__device__ void bracket_pass(int n, KeyOf key_of, PiOf pi_of, uint32_t k, const Fx &T, Red &R,
+                             const Fx *T_keep_all = nullptr) {
+  SearchState &st = R.sm.st;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t l = st.l, r = st.r, cr = st.cr;
+  const int sh = bracket_shift(r - l);
+  R.hcnt[tid] = 0u;
+  if (MASS) {
+#pragma unroll
+    for (int q = 0; q < 5; ++q) R.hms[q * kBins + tid] = 0ull;
+  }
+  __syncthreads();
+  for (int i = tid; i < n; i += kThreads) {
+    uint32_t key;
+    if (!key_of(i, key)) continue;
+    if (key <= l || key > r) continue;
+    const uint32_t b = (key - l - 1u) >> sh;
+    atomicAdd(&R.hcnt[b], 1u);
+    if (MASS) {
+      const Fx f = fx_from_double(pi_of(i));
+      const uint32_t pc[5] = {(uint32_t)f.w0, (uint32_t)(f.w0 >> 32), (uint32_t)f.w1,
+                              (uint32_t)(f.w1 >> 32), (uint32_t)f.w2};
+#pragma unroll
+      for (int q = 0; q < 5; ++q)
+        if (pc[q]) atomicAdd(&R.hms[q * kBins + b], (unsigned long long)pc[q]);
+    }
+  }
+  __syncthreads();
+  // suffix scan over buckets: thread t holds bucket b = 255 - t, so a prefix over t is a suffix over b
+  const int b = kBins - 1 - tid;
+  const uint32_t c = R.hcnt[b];
+  uint32_t ci = c;
+  Fx m = fx_zero(), mi = fx_zero();
+  if (MASS) {
+    // normalise the 32-bit pieces (each container < 2^42) into one 192-bit value
+    unsigned long long carry = 0ull;
+    uint32_t pw[5];
+#pragma unroll
+    for (int q = 0; q < 5; ++q) {
+      const unsigned long long v = R.hms[q * kBins + b] + carry;
+      pw[q] = (uint32_t)v;
+      carry = v >> 32;
+    }
+    m = Fx{(unsigned long long)pw[0] | ((unsigned long long)pw[1] << 32),
+           (unsigned long long)pw[2] | ((unsigned long long)pw[3] << 32),
+           (unsigned long long)pw[4] + (carry << 32)};
+    mi = m;
+  }
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t cv = __shfl_up_sync(0xffffffffu, ci, o);
+    if (lane >= o) ci += cv;
+    if (MASS) {
+      Fx mv;
+      mv.w0 = __shfl_up_sync(0xffffffffu, mi.w0, o);
+      mv.w1 = __shfl_up_sync(0xffffffffu, mi.w1, o);
+      mv.w2 = __shfl_up_sync(0xffffffffu, mi.w2, o);
+      if (lane >= o) mi = fx_add(mi, mv);
+    }
+  }
+  if (lane == 31) {
+    R.sm.ctot[warp] = ci;
+    if (MASS) R.sm.mtot[warp] = mi;
+  }
+  __syncthreads();
+  uint32_t above = cr;  // keys above this warp's buckets (higher buckets live in lower warps)
+  Fx mab = st.Mr;
+  for (int w = 0; w < warp; ++w) {
+    above += R.sm.ctot[w];
+    if (MASS) mab = fx_add(mab, R.sm.mtot[w]);
+  }
+  const uint32_t suf = above + ci;          // keys in buckets >= b, plus everything above r
+  const uint32_t suf_hi = suf - c;          // keys in buckets > b
+  const Fx msuf = MASS ? fx_add(mab, mi) : fx_zero();
+  const Fx msuf_hi = MASS ? fx_sub(msuf, m) : fx_zero();
+  if (MASS && T_keep_all && b == 0) {  // everything in range: the survivors' total
+    st.Ml = msuf;
+    st.cl = suf;
+    st.compact = fx_ge(msuf, *T_keep_all) ? 0 : 2;  // 2 = keep all
+  }
+  __syncthreads();
+  if (MASS && T_keep_all && st.compact == 2) return;
+  // the crossing bucket: reaches the target with itself, misses it without
+  const bool in = MASS ? fx_ge(msuf, T) : (suf >= k);
+  const bool hi_in = MASS ? fx_ge(msuf_hi, T) : (suf_hi >= k);
+  if (in && !hi_in && c > 0u) {
+    const uint32_t lo_b = l + ((uint32_t)b << sh);
+    const unsigned long long hi_b = (unsigned long long)l + ((unsigned long long)(b + 1) << sh);
+    st.l = lo_b;
+    st.cl = suf;
+    st.r = hi_b < (unsigned long long)r ? (uint32_t)hi_b : r;
+    st.cr = suf_hi;
+    if (MASS) { st.Ml = msuf; st.Mr = msuf_hi; }
+    if (sh == 0) {  // single-key bucket: done
+      st.done = 1u; st.K = lo_b + 1u; st.n_gt = suf_hi; st.n_eq = c;
+      if (MASS) st.H = msuf_hi;
+    }
+    st.iters += 1;
+  }
+  __syncthreads();
+}
+
 template <int NP, class Src>
 __device__ KRes search_k(const Src &src, uint32_t l, uint32_t r, uint32_t cl, uint32_t cr, uint32_t k,
                          Red &R) {
@@ -509,6 +659,18 @@ __device__ KRes search_k(const Src &src, uint32_t l, uint32_t r, uint32_t cl, ui
   }
   __syncthreads();
   const Fx zero = fx_zero();
+  if (r - l > (uint32_t)(4 * kBins)) {
+    bracket_pass<false>(src.n, [&](int i, uint32_t &key) {
+      uint32_t bits, ix;
+      src.get(i, bits, ix);
+      key = key_of_bits(bits);
+      return true; }, [&](int) { return 0.0; }, k, zero, R);
+    if (threadIdx.x == 0 && !st.done) {
+      const uint32_t n_in = st.cl - st.cr;
+      if ((int)n_in <= R.act_cap_k && 2 * (int)n_in <= src.n) st.compact = 1;
+    }
+    __syncthreads();
+  }
   bool act = false;  // searching the compacted active set instead of src
   for (;;) {
     l = st.l; r = st.r; cr = st.cr;
@@ -590,20 +752,61 @@ struct PRes {
   uint32_t n_eq;   // survivors equal to K
   Fx H;            // exact mass strictly above K
   int iters;
+  bool keep_all;   // p >= fsum(all survivors): no truncation (oracle.py:45-46)
+  Fx total;        // exact mass of all survivors
 };
 
 // Top-p boundary search.  Restates _search_topp + _resolve_topp (pivot_search.py:159-232) with logit
 // keys as pivots and exact masses: the crossing cluster (fsum(head) < p <= fsum(head + cluster),
 // pivot_search.py:177-191) is found directly, no resolve walk.  Invariant: M(l) >= T > M(r).
+// The survivors' total mass is computed here (by the bracketing pass when the range is wide, else by
+// one reduction); when p >= fsum(total) the result is keep_all.
 template <int NP, class Src, class InS, class PiOf, class PiKey>
-__device__ PRes search_p(const Src &src, uint32_t l, uint32_t r, uint32_t cl, uint32_t cr, Fx Ml, Fx Mr,
-                         const Fx &T, InS in_s, PiOf pi_of, PiKey pi_key, Red &R) {
+__device__ PRes search_p(const Src &src, uint32_t l, uint32_t r, const Fx &T, const Fx &Tsp, InS in_s,
+                         PiOf pi_of, PiKey pi_key, Red &R) {
   SearchState &st = R.sm.st;
+  uint32_t cl = 0u, cr = 0u;
+  Fx Ml = fx_zero(), Mr = fx_zero();
   if (threadIdx.x == 0) {
-    st.l = l; st.r = r; st.cl = cl; st.cr = cr; st.Ml = Ml; st.Mr = Mr; st.done = 0u; st.iters = 0;
+    st.l = l; st.r = r; st.cl = 0u; st.cr = 0u; st.Ml = Ml; st.Mr = Mr; st.done = 0u; st.iters = 0;
     st.compact = 0; st.n_act = 0u;
   }
   __syncthreads();
+  if (r - l > (uint32_t)(4 * kBins)) {
+    bracket_pass<true>(src.n, [&](int i, uint32_t &key) {
+      uint32_t bits, ix;
+      src.get(i, bits, ix);
+      key = key_of_bits(bits);
+      return in_s(key, ix); }, [&](int i) {
+      uint32_t bits, ix;
+      src.get(i, bits, ix);
+      return pi_of(bits, i); }, 0u, T, R, &Tsp);
+    if (st.compact == 2) {  // keep everything
+      PRes res{};
+      res.keep_all = true;
+      res.total = st.Ml;
+      __syncthreads();
+      return res;
+    }
+    if (threadIdx.x == 0 && !st.done) {
+      const uint32_t n_in = st.cl - st.cr;
+      if ((int)n_in <= R.act_cap_p && 2 * (int)n_in <= src.n) st.compact = 1;
+    }
+    __syncthreads();
+  } else {
+    uint32_t cnt;
+    const Fx tot = block_mass(src, [&](uint32_t bits, uint32_t ix, int i, double &v) {
+      if (!in_s(key_of_bits(bits), ix)) return false;
+      v = pi_of(bits, i); return true; }, cnt, R);
+    if (!fx_ge(tot, Tsp)) {
+      PRes res{};
+      res.keep_all = true;
+      res.total = tot;
+      return res;
+    }
+    if (threadIdx.x == 0) { st.cl = cnt; st.Ml = tot; }
+    __syncthreads();
+  }
   bool act = false;
   for (;;) {
     l = st.l; r = st.r; cr = st.cr;
@@ -689,8 +892,8 @@ __device__ PRes search_p(const Src &src, uint32_t l, uint32_t r, uint32_t cl, ui
     }
     __syncthreads();
   }
-  const PRes res = st.done ? PRes{st.K, st.n_gt, st.n_eq, st.H, st.iters}
-                           : PRes{st.r, st.cr, st.cl - st.cr, st.Mr, st.iters};
+  const PRes res = st.done ? PRes{st.K, st.n_gt, st.n_eq, st.H, st.iters, false, fx_zero()}
+                           : PRes{st.r, st.cr, st.cl - st.cr, st.Mr, st.iters, false, fx_zero()};
   __syncthreads();
   return res;
 }
@@ -767,22 +970,6 @@ __device__ __forceinline__ bool kept_by(uint32_t key, uint32_t idx, uint32_t K, 
   return key > K || (key == K && idx <= cut);
 }
 
-// Exact block-wide sum of fx(v) over the elements accepted by fn(bits, idx, i, v); also counts them.
-template <class Src, class Fn>
-__device__ Fx block_mass(const Src &src, Fn fn, uint32_t &count, Red &R) {
-  Buckets<1, true> b;
-  b.cnt[0] = 0u; b.mn[0] = 0u; b.mc[0] = 0u; b.ms[0] = fx_zero();
-  for (int i = threadIdx.x; i < src.n; i += kThreads) {
-    uint32_t bits, ix;
-    src.get(i, bits, ix);
-    double v;
-    if (fn(bits, ix, i, v)) { b.ms[0] = fx_add(b.ms[0], fx_from_double(v)); b.cnt[0] += 1u; }
-  }
-  bk_reduce(b, R);
-  count = b.cnt[0];
-  return b.ms[0];
-}
-
 // Full-row output pass.  how: 0 = kept values only (background already -inf), 1 = every element,
 // 2 = -inf where not kept (in-place).
 template <typename T>
@@ -797,13 +984,23 @@ __device__ void write_row(const T *in, T *out, int V, uint32_t K, uint32_t cut, 
 }
 
 template <typename T, int NP>
-__global__ void __launch_bounds__(kThreads) qrita_tail(Params P) {
+__global__ void __launch_bounds__(kThreads, 2) qrita_tail(Params P) {
   extern __shared__ __align__(16) uint8_t dsmem[];
   __shared__ TailSmem sm;
   __shared__ uint32_t s_off[kMaxTailChunks + 1];
   __shared__ uint32_t s_part[2][kWarps][5];
   pdl_wait();  // outliers and chunk statistics of qrita_stream (and plans of qrita_prep)
   const int row = blockIdx.x;
+  const bool dbg = (P.flags & QRITA_DEBUG_TIMING) != 0;
+#define QRITA_TSTAMP(i)                                                                 \
+  do {                                                                                  \
+    if (dbg && threadIdx.x == 0) {                                                      \
+      unsigned long long t_;                                                            \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                            \
+      P.dbg[(size_t)blockIdx.x * 16 + (i)] = t_;                                        \
+    }                                                                                   \
+  } while (0)
+  QRITA_TSTAMP(0);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int V = P.V;
   const int nch = P.nchunks;
@@ -859,6 +1056,7 @@ __global__ void __launch_bounds__(kThreads) qrita_tail(Params P) {
   const bool overflow = ovf != 0u || nch > kMaxTailChunks;
   const uint32_t lo_row = minkey ? minkey - 1u : 0u;  // below every key of the row
   __syncthreads();
+  QRITA_TSTAMP(1);
 
   qrita_row_metrics met;
   memset(&met, 0, sizeof(met));
@@ -894,16 +1092,35 @@ __global__ void __launch_bounds__(kThreads) qrita_tail(Params P) {
   // ---- stage the outliers in shared memory (index order) when they fit
   const bool x_fits = sigma && !overflow && n_c <= (uint32_t)kCapX;
   if (x_fits) {
-    for (int c = warp; c < nch; c += kWarps) {  // one warp per chunk: coalesced slot reads
+    // one thread per chunk: 16-byte loads straight from the chunk's slots (slots are 1 KB aligned),
+    // all issued before the shared-memory stores
+    for (int c = tid; c < nch; c += kThreads) {
       const uint32_t off = s_off[c], cc = s_off[c + 1] - off;
       const size_t slot = ((size_t)row * nch + c) * kCapChunk;
-      for (uint32_t j = lane; j < cc; j += 32) {
-        xb[off + j] = __ldcg(P.cand_bits + slot + j);
-        xi[off + j] = __ldcg(P.cand_idx + slot + j);
+      const uint4 *pb = reinterpret_cast<const uint4 *>(P.cand_bits + slot);
+      const uint4 *pi = reinterpret_cast<const uint4 *>(P.cand_idx + slot);
+      for (uint32_t j0 = 0; j0 < cc; j0 += 32u) {
+        uint4 qb[8], qi[8];
+#pragma unroll
+        for (int g = 0; g < 8; ++g) {
+          if (j0 + 4u * g < cc) { qb[g] = __ldcg(pb + (j0 >> 2) + g); qi[g] = __ldcg(pi + (j0 >> 2) + g); }
+        }
+#pragma unroll
+        for (int g = 0; g < 8; ++g) {
+          const uint32_t j = j0 + 4u * g;
+          if (j < cc) {
+            const uint32_t vb[4] = {qb[g].x, qb[g].y, qb[g].z, qb[g].w};
+            const uint32_t vi[4] = {qi[g].x, qi[g].y, qi[g].z, qi[g].w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+              if (j + e < cc) { xb[off + j + e] = vb[e]; xi[off + j + e] = vi[e]; }
+          }
+        }
       }
     }
     __syncthreads();
   }
+  QRITA_TSTAMP(2);
   const SrcX X{xb, xi, (int)n_c};
   const SrcRow<T> RW{in, V};
   Red red(sm);
@@ -911,6 +1128,8 @@ __global__ void __launch_bounds__(kThreads) qrita_tail(Params P) {
   red.act_pi = ap;
   red.act_cap_k = 3 * kCapA;
   red.act_cap_p = kCapA;
+  red.hms = (unsigned long long *)ap;               // 5 * kBins * 8 B = 10 KB
+  red.hcnt = (uint32_t *)(red.hms + 5 * kBins);     // + 1 KB  (region: 12 KB)
 
   uint32_t Kf = 0u, cutf = kNoCut, kept = (uint32_t)V;
   bool k_used_x = false;  // the final kept set is a subset of X
@@ -932,6 +1151,7 @@ __global__ void __launch_bounds__(kThreads) qrita_tail(Params P) {
       full_row = true;
     }
     met.k_search_iters = kr.iters;
+    QRITA_TSTAMP(3);
     Kk = kr.K;
     uint32_t ck = k - kr.n_gt;  // n_keep = n_dup - (N - k), pipeline.py:117
     if (nodup) ck = kr.n_eq;
@@ -939,6 +1159,7 @@ __global__ void __launch_bounds__(kThreads) qrita_tail(Params P) {
     else cutk = k_used_x ? select_nth_eq(X, Kk, ck, red) : select_nth_eq(RW, Kk, ck, red);
     n_s = kr.n_gt + ck;
     Kf = Kk; cutf = cutk; kept = n_s;
+    QRITA_TSTAMP(4);
   }
 
   // ================= top-p stage: pipeline.py:161-196 (p only) and :226-239 (k then p) ============
@@ -958,12 +1179,12 @@ __global__ void __launch_bounds__(kThreads) qrita_tail(Params P) {
       // compact S into shared memory with its exp values (order is irrelevant: sums are exact)
       if (tid == 0) sm.u[4] = 0u;
       __syncthreads();
-      for (int i = tid; i < X.n; i += kThreads) {
-        const uint32_t b = xb[i];
-        if (kept_by(key_of_bits(b), xi[i], Kk, cutk)) {
-          const uint32_t pos = atomicAdd(&sm.u[4], 1u);
-          sb[pos] = b; si[pos] = xi[i]; sp[pos] = e_of(b);
-        }
+      for (int i0 = 0; i0 < X.n; i0 += kThreads) {
+        const int i = i0 + tid;
+        const uint32_t b = i < X.n ? xb[i] : 0u;
+        const bool in = i < X.n && kept_by(key_of_bits(b), xi[i], Kk, cutk);
+        const uint32_t pos = warp_reserve(&sm.u[4], in);
+        if (in) { sb[pos] = b; si[pos] = xi[i]; sp[pos] = e_of(b); }
       }
       __syncthreads();
       ns_cached = sm.u[4];
@@ -986,18 +1207,18 @@ __global__ void __launch_bounds__(kThreads) qrita_tail(Params P) {
       D = fx_to_double(Dx);
       full_row = true;
     }
+    QRITA_TSTAMP(5);
     auto pi_bits = [&](uint32_t bits) -> double { return e_of(bits) / D; };
     auto pi_key = [&](uint32_t key) -> double { return pi_bits(bits_of_key(key)); };
 
     // ---- pick the set the nucleus search runs on: 0 = cached S, 1 = X (filtered), 2 = full row
     int set_kind;
-    uint32_t l0, cl0;
-    Fx Ml0;
+    uint32_t l0;
     if (topp_only) {
       // sigma hit for top-p: outlier mass > p (is_hit, sigma_trunc.py:134-138), judged exactly
       bool hit_ref = false;
-      Fx Mx = fx_zero();
       if (sigma) {
+        Fx Mx;
         if (x_fits) {
           Mx = block_mass(X, [&](uint32_t b, uint32_t, int, double &v) { v = pi_bits(b); return true; }, cnt_dummy, red);
         } else {
@@ -1011,47 +1232,33 @@ __global__ void __launch_bounds__(kThreads) qrita_tail(Params P) {
       met.trunc_hit = (hit_ref && !force_fb) ? 1 : 0;
       met.fallback_used = met.trunc_hit ? 0 : 1;
       if (met.trunc_hit && x_fits) {
-        set_kind = 1; l0 = pl.key_thr ? pl.key_thr - 1u : 0u; cl0 = n_c; Ml0 = Mx;
+        set_kind = 1; l0 = pl.key_thr ? pl.key_thr - 1u : 0u;
       } else {
-        set_kind = 2; l0 = lo_row; cl0 = (uint32_t)V;
-        Ml0 = block_mass(RW, [&](uint32_t b, uint32_t, int, double &v) { v = pi_bits(b); return true; }, cnt_dummy, red);
+        set_kind = 2; l0 = lo_row;
         full_row = true;
       }
-    } else if (s_cached) {
-      set_kind = 0; l0 = Kk - 1u; cl0 = ns_cached;  // every survivor has key >= Kk
-      const SrcX S{sb, si, (int)ns_cached};
-      Ml0 = block_mass(S, [&](uint32_t, uint32_t, int i, double &v) { v = sp[i]; return true; }, cnt_dummy, red);
-    } else if (k_used_x) {
-      set_kind = 1; l0 = Kk - 1u; cl0 = n_s;
-      Ml0 = block_mass(X, [&](uint32_t b, uint32_t ix, int, double &v) {
-        if (!kept_by(key_of_bits(b), ix, Kk, cutk)) return false;
-        v = pi_bits(b); return true; }, cnt_dummy, red);
     } else {
-      set_kind = 2; l0 = Kk - 1u; cl0 = n_s;
-      Ml0 = block_mass(RW, [&](uint32_t b, uint32_t ix, int, double &v) {
-        if (!in_s(key_of_bits(b), ix)) return false;
-        v = pi_bits(b); return true; }, cnt_dummy, red);
+      set_kind = s_cached ? 0 : (k_used_x ? 1 : 2);
+      l0 = Kk - 1u;  // every survivor has key >= Kk
     }
 
-    if (!fx_ge(Ml0, Tsp)) {
+    QRITA_TSTAMP(6);
+    PRes pr;
+    if (set_kind == 0) {
+      const SrcX S{sb, si, (int)ns_cached};
+      pr = search_p<NP>(S, l0, maxkey, Tp, Tsp, [&](uint32_t, uint32_t) { return true; },
+                        [&](uint32_t, int i) { return sp[i]; }, pi_key, red);
+    } else if (set_kind == 1) {
+      pr = search_p<NP>(X, l0, maxkey, Tp, Tsp, in_s, [&](uint32_t b, int) { return pi_bits(b); }, pi_key, red);
+    } else {
+      pr = search_p<NP>(RW, l0, maxkey, Tp, Tsp, in_s, [&](uint32_t b, int) { return pi_bits(b); }, pi_key, red);
+    }
+    if (pr.keep_all) {
       // p >= fsum(all survivors): keep them all (oracle.py:45-46)
       if (topp_only) { Kf = 0u; cutf = kNoCut; kept = (uint32_t)V; }
     } else {
-      PRes pr;
-      const Fx zero = fx_zero();
-      if (set_kind == 0) {
-        const SrcX S{sb, si, (int)ns_cached};
-        pr = search_p<NP>(S, l0, maxkey, cl0, 0u, Ml0, zero, Tp,
-                          [&](uint32_t, uint32_t) { return true; },
-                          [&](uint32_t, int i) { return sp[i]; }, pi_key, red);
-      } else if (set_kind == 1) {
-        pr = search_p<NP>(X, l0, maxkey, cl0, 0u, Ml0, zero, Tp, in_s,
-                          [&](uint32_t b, int) { return pi_bits(b); }, pi_key, red);
-      } else {
-        pr = search_p<NP>(RW, l0, maxkey, cl0, 0u, Ml0, zero, Tp, in_s,
-                          [&](uint32_t b, int) { return pi_bits(b); }, pi_key, red);
-      }
       met.p_search_iters = pr.iters;
+      QRITA_TSTAMP(7);
       // smallest j with fsum(head + j * p_b) >= p (_min_dup_count, pivot_search.py:143-156), exactly
       if (tid == 0) {
         const double pb = pi_key(pr.K);
@@ -1080,6 +1287,7 @@ __global__ void __launch_bounds__(kThreads) qrita_tail(Params P) {
     }
   }
 
+  QRITA_TSTAMP(8);
   // ================= output: finalize_mask, pipeline.py:60-78 =================
   if (mode == MODE_TOPP) {
     write_row<T>(in, out, V, Kf, cutf, inplace ? 2 : 1);  // the stream left top-p-only rows alone
@@ -1093,6 +1301,7 @@ __global__ void __launch_bounds__(kThreads) qrita_tail(Params P) {
   } else {
     write_row<T>(in, out, V, Kf, cutf, 0);
   }
+  QRITA_TSTAMP(9);
   if (tid == 0) {
     met.kept_count = (int32_t)kept;
     met.full_row_path = full_row ? 1 : 0;
@@ -1197,7 +1406,8 @@ __global__ void __launch_bounds__(kStreamThreads, 3) qrita_stream(Params P) {
     const float thr = plp->has_thr ? __uint_as_float(bits_of_key(plp->key_thr)) : qnan;
     const bool write_bg = !inplace && (mode == MODE_TOPK || mode == MODE_TOPKP || mode == MODE_INVALID);
     const bool write_copy = !inplace && mode == MODE_PASS;
-    float fmx = __uint_as_float(0xff800000u), fmn = __uint_as_float(0x7f800000u);
+    // finite identities, so lanes without elements (ragged chunks) never look non-finite
+    float fmx = -3.402823466e38f, fmn = 3.402823466e38f;
     uint32_t base = 0u;
     if (whole) {
 #pragma unroll

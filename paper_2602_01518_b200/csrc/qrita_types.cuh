@@ -80,6 +80,7 @@ struct Params {
   uint32_t *cand_idx;
   int32_t *status;
   int32_t *nf_col;
+  unsigned long long *dbg;  // [B][16] phase timestamps of the row tail (QRITA_DEBUG_TIMING)
   int nchunks;
   int total_items;
   PwTree tree;
@@ -89,7 +90,7 @@ struct Params {
 // rewritten by each call (no state carries over), and the status block only depends on B, so
 // qrita_get_status needs no V.
 struct WsLayout {
-  size_t status, nf_col, plans, cstats, cand_bits, cand_idx, total;
+  size_t status, nf_col, dbg, plans, cstats, cand_bits, cand_idx, total;
 };
 
 inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
@@ -100,6 +101,7 @@ inline WsLayout ws_layout(int B, int V) {
   size_t off = 0;
   L.status = off;    off = align_up(off + 4ull * (size_t)B, 256);
   L.nf_col = off;    off = align_up(off + 4ull * (size_t)B, 256);
+  L.dbg = off;       off = align_up(off + 128ull * (size_t)B, 256);
   L.plans = off;     off = align_up(off + sizeof(RowPlan) * (size_t)B, 256);
   L.cstats = off;    off = align_up(off + sizeof(ChunkStat) * (size_t)B * nchunks, 256);
   L.cand_bits = off; off = align_up(off + 4ull * (size_t)B * nchunks * kCapChunk, 256);

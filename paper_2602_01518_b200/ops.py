@@ -29,6 +29,7 @@ class TruncFlags:
     use_sigma_trunc: bool = True
     force_fallback: bool = False
     dup_handling: bool = True
+    debug_timing: bool = False          # record tail phase timestamps (qrita_get_timing)
 
     def bits(self) -> int:
         if self.search not in ("quaternary", "binary"):
@@ -42,6 +43,8 @@ class TruncFlags:
             f |= N.FORCE_FALLBACK
         if not self.dup_handling:
             f |= N.NO_DUP
+        if self.debug_timing:
+            f |= N.DEBUG_TIMING
         return f
 
 

@@ -69,3 +69,33 @@ if len(sys.argv) > 1 and sys.argv[1] == "stats":
         for f in ("trunc_hit", "outlier_count", "k_search_iters", "p_search_iters", "kept_count", "full_row_path"):
             vals = [r[f] for r in m]
             print(f"{cfg} {f}: mean {st.mean(vals):.2f} max {max(vals)}")
+
+if len(sys.argv) > 1 and sys.argv[1] == "timing":
+    import bench, ctypes
+    from paper_2602_01518_b200 import _native as N
+    for cfg in sys.argv[2:]:
+        x, k, p, dtype, desc = bench.workload(cfg)
+        tdt = torch.bfloat16 if dtype == "bf16" else torch.float32
+        xt = torch.from_numpy(x).cuda().to(tdt)
+        kt, pt = torch.from_numpy(k).cuda(), torch.from_numpy(p).cuda()
+        fl = Q.TruncFlags(debug_timing=True)
+        for _ in range(3):
+            Q.topk_topp(xt, kt, pt, flags=fl)
+        torch.cuda.synchronize()
+        st = torch.cuda.current_stream()
+        ws = Q.ops.workspace_for(xt.device, st)
+        ptr, _ = ws.get(0, st)
+        B = x.shape[0]
+        buf = (ctypes.c_ulonglong * (16 * B))()
+        N.load().qrita_get_timing(ctypes.c_void_p(ptr), B, buf, ctypes.c_void_p(st.cuda_stream))
+        a = np.frombuffer(buf, dtype=np.uint64).reshape(B, 16).astype(np.int64)
+        t0 = a[:, 0]
+        print(f"{cfg}: tail start spread {(t0.max()-t0.min())/1e3:.1f} us; total tail span {(a[:,9].max()-t0.min())/1e3:.1f} us")
+        names = ["stats", "stageX", "ksearch", "kcut", "S+D", "Ml0", "psearch", "pcut", "output"]
+        prev = a[:, 0]
+        for i, nm in enumerate(names, start=1):
+            cur = a[:, i]
+            ok = cur > 0
+            d = np.where(ok, cur - prev, 0)
+            print(f"   {nm:8s} mean {d[ok].mean()/1e3 if ok.any() else 0:7.2f} us  max {d.max()/1e3:7.2f}")
+            prev = np.where(ok, cur, prev)
