@@ -227,12 +227,12 @@ def main():
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
     st = torch.cuda.current_stream(dev)
 
-    def step(ev0, ev1, ev2):
+    def step(ev0, ev1):
         ev0.record(st)
-        Q.topk_topp(x, k, p, out=out, check=False, prep_event=ev1)
-        ev2.record(st)
+        Q.topk_topp(x, k, p, out=out, check=False)
+        ev1.record(st)
 
-    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(args.steps)]
     for _ in range(args.warmup):
         flush.zero_()
         Q.topk_topp(x, k, p, out=out, check=True)
@@ -247,9 +247,7 @@ def main():
         torch.cuda.synchronize(dev)
     if world > 1:
         dist.barrier()
-    step_ms = [a.elapsed_time(c) for a, _, c in evs]
-    main_ms = [bb.elapsed_time(c) for _, bb, c in evs]
-    prep_ms = [a.elapsed_time(bb) for a, bb, _ in evs]
+    step_ms = [a.elapsed_time(c) for a, c in evs]
     total_ms = sum(step_ms)
     if world > 1:
         t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
@@ -258,15 +256,27 @@ def main():
     value = world * b * args.steps / (total_ms / 1e3)
     ms_per_step = total_ms / args.steps
 
-    # roofline of the dominant kernel (qrita_main): 1 read + 1 write of the [B, V] matrix
+    # per-kernel times (profiling iterations, untimed above): the events serialise the launches, so
+    # prep / stream / tail are each measured alone on the launching stream
+    prof = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(max(5, min(args.steps, 20)))]
+    for e0, e1, e2, e3 in prof:
+        flush.zero_()
+        e0.record(st)
+        Q.topk_topp(x, k, p, out=out, check=False, prep_event=e1, stream_event=e2)
+        e3.record(st)
+    torch.cuda.synchronize(dev)
+    prep_ms = statistics.mean(a.elapsed_time(bb) for a, bb, _, _ in prof)
+    stream_ms = statistics.mean(bb.elapsed_time(c) for _, bb, c, _ in prof)
+    tail_ms = statistics.mean(c.elapsed_time(d) for _, _, c, d in prof)
+
+    # roofline of the dominant kernel (qrita_stream: 1 read + 1 write of the [B, V] matrix)
     alg_bytes = b * v * esize * 2
-    main_avg_s = statistics.mean(main_ms) / 1e3
-    achieved = alg_bytes / main_avg_s / 1e9
+    achieved = alg_bytes / (stream_ms / 1e3) / 1e9
     peak, peak_kind = measured_peak()
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": ncu_traffic(args.config),
-                "peak_source": peak_kind, "kernel": "qrita_main",
-                "kernel_ms": statistics.mean(main_ms), "prep_ms": statistics.mean(prep_ms),
+                "peak_source": peak_kind, "kernel": "qrita_stream",
+                "kernel_ms": stream_ms, "prep_ms": prep_ms, "tail_ms_serialised": tail_ms,
                 "alg_bytes_per_launch": alg_bytes,
                 "step_frac": alg_bytes / (ms_per_step / 1e3) / 1e9 / peak}
 

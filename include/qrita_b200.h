@@ -107,15 +107,16 @@ int qrita_topk_topp(const void *logits, int64_t ld_in, int dtype, int B, int V,
                     void *workspace, size_t ws_bytes, int flags, int sample_size,
                     qrita_stream_t stream);
 
-/* Same as qrita_topk_topp; additionally records `prep_done_event` (a cudaEvent_t, may be NULL) on
- * `stream` between the per-row preparation kernel and the streaming/search kernel, so a caller can
- * time the two launches separately with events (bench.py's roofline measurement). */
+/* Same as qrita_topk_topp, for profiling: records `prep_done_event` after the preparation kernel and
+ * `stream_done_event` after the streaming kernel (cudaEvent_t each, may be NULL).  A non-NULL event
+ * serialises the launches around it (no programmatic overlap), so each kernel can be timed alone
+ * with events (bench.py's roofline measurement). */
 int qrita_topk_topp_ex(const void *logits, int64_t ld_in, int dtype, int B, int V,
                        const int64_t *k, const double *p,
                        void *out, int64_t ld_out,
                        int32_t *kept_count, qrita_row_metrics *metrics,
                        void *workspace, size_t ws_bytes, int flags, int sample_size,
-                       qrita_stream_t stream, void *prep_done_event);
+                       qrita_stream_t stream, void *prep_done_event, void *stream_done_event);
 
 /* Synchronises `stream`, then reports the first failing row of the last call on this workspace:
  * returns QRITA_OK or QRITA_EINVAL_K / QRITA_EINVAL_P / QRITA_ENONFINITE, and fills *row / *col

@@ -81,7 +81,7 @@ def load() -> ctypes.CDLL:
     lib.qrita_topk_topp.argtypes = [vp, i64, i32, i32, i32, vp, vp, vp, i64, vp, vp, vp, sz, i32, i32, vp]
     lib.qrita_topk_topp.restype = i32
     lib.qrita_topk_topp_ex.argtypes = [vp, i64, i32, i32, i32, vp, vp, vp, i64, vp, vp, vp, sz, i32, i32,
-                                       vp, vp]
+                                       vp, vp, vp]
     lib.qrita_topk_topp_ex.restype = i32
     lib.qrita_get_status.argtypes = [vp, i32, ctypes.POINTER(i32), ctypes.POINTER(i32), vp]
     lib.qrita_get_status.restype = i32

@@ -91,14 +91,14 @@ int qrita_topk_topp(const void *logits, int64_t ld_in, int dtype, int B, int V,
                     void *workspace, size_t ws_bytes, int flags, int sample_size,
                     qrita_stream_t stream) {
   return qrita_topk_topp_ex(logits, ld_in, dtype, B, V, k, p, out, ld_out, kept_count, metrics,
-                            workspace, ws_bytes, flags, sample_size, stream, NULL);
+                            workspace, ws_bytes, flags, sample_size, stream, NULL, NULL);
 }
 
 int qrita_topk_topp_ex(const void *logits, int64_t ld_in, int dtype, int B, int V,
                        const int64_t *k, const double *p, void *out, int64_t ld_out,
                        int32_t *kept_count, qrita_row_metrics *metrics,
                        void *workspace, size_t ws_bytes, int flags, int sample_size,
-                       qrita_stream_t stream, void *prep_done_event) {
+                       qrita_stream_t stream, void *prep_done_event, void *stream_done_event) {
   if (!logits || !out || !k || !p || !workspace) return QRITA_EINVAL_ARG;
   if (B < 1 || V < 1 || ld_in < V || ld_out < V || sample_size < 1) return QRITA_EINVAL_ARG;
   if (dtype != QRITA_DTYPE_F32 && dtype != QRITA_DTYPE_BF16) return QRITA_EINVAL_ARG;
@@ -126,6 +126,7 @@ int qrita_topk_topp_ex(const void *logits, int64_t ld_in, int dtype, int B, int 
   P.status = (int32_t *)(ws + L.status);
   P.nf_col = (int32_t *)(ws + L.nf_col);
   P.dbg = (unsigned long long *)(ws + L.dbg);
+  P.row_done = (uint32_t *)(ws + L.row_done);
   P.nchunks = (int)nchunks;
   P.total_items = (int)((size_t)B * nchunks);
   pw_tree(sample_size < V ? sample_size : V, P.tree);
@@ -134,8 +135,10 @@ int qrita_topk_topp_ex(const void *logits, int64_t ld_in, int dtype, int B, int 
   const bool vec = ((uintptr_t)logits % 16 == 0) && ((uintptr_t)out % 16 == 0) &&
                    ((size_t)ld_in * es % 16 == 0) && ((size_t)ld_out * es % 16 == 0);
   cudaError_t e = dtype == QRITA_DTYPE_F32
-                      ? launch_f32(P, (cudaStream_t)stream, vec, (cudaEvent_t)prep_done_event)
-                      : launch_bf16(P, (cudaStream_t)stream, vec, (cudaEvent_t)prep_done_event);
+                      ? launch_f32(P, (cudaStream_t)stream, vec, (cudaEvent_t)prep_done_event,
+                                   (cudaEvent_t)stream_done_event)
+                      : launch_bf16(P, (cudaStream_t)stream, vec, (cudaEvent_t)prep_done_event,
+                                    (cudaEvent_t)stream_done_event);
   return e == cudaSuccess ? QRITA_OK : QRITA_ECUDA;
 }
 

@@ -310,10 +310,11 @@ __global__ void __launch_bounds__(256) qrita_prep(Params P) {
       pl.t_sp = fx_zero();
     }
     pl.has_thr = want_thr ? 1 : 0;
-    pl.pad = 0;
+    pl.pad[0] = pl.pad[1] = pl.pad[2] = 0;
     P.plans[row] = pl;
     P.status[row] = (bad_k ? ST_BAD_K : 0) | (bad_p ? ST_BAD_P : 0);
     P.nf_col[row] = -1;
+    P.row_done[row] = 0u;
   }
 }
 
@@ -984,13 +985,15 @@ __device__ void write_row(const T *in, T *out, int V, uint32_t K, uint32_t cut, 
 }
 
 template <typename T, int NP>
-__global__ void __launch_bounds__(kThreads, 2) qrita_tail(Params P) {
-  extern __shared__ __align__(16) uint8_t dsmem[];
-  __shared__ TailSmem sm;
-  __shared__ uint32_t s_off[kMaxTailChunks + 1];
-  __shared__ uint32_t s_part[2][kWarps][5];
-  pdl_wait();  // outliers and chunk statistics of qrita_stream (and plans of qrita_prep)
+__device__ __forceinline__ void tail_body(const Params &P, uint8_t *dsmem, TailSmem &sm, uint32_t *s_off,
+                                          uint32_t (*s_part)[kWarps][5]) {
   const int row = blockIdx.x;
+  // Runs concurrently with qrita_stream (programmatic launch): wait for this row's chunks only.
+  if (threadIdx.x == 0) {
+    const uint32_t need = (uint32_t)P.nchunks;
+    while (ld_acquire_gpu(P.row_done + row) < need) __nanosleep(256);
+  }
+  __syncthreads();
   const bool dbg = (P.flags & QRITA_DEBUG_TIMING) != 0;
 #define QRITA_TSTAMP(i)                                                                 \
   do {                                                                                  \
@@ -1004,7 +1007,13 @@ __global__ void __launch_bounds__(kThreads, 2) qrita_tail(Params P) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int V = P.V;
   const int nch = P.nchunks;
-  const RowPlan pl = P.plans[row];
+  RowPlan pl;
+  {
+    const uint4 *src4 = reinterpret_cast<const uint4 *>(P.plans + row);
+    uint4 *dst4 = reinterpret_cast<uint4 *>(&pl);
+#pragma unroll
+    for (int i = 0; i < (int)(sizeof(RowPlan) / 16); ++i) dst4[i] = __ldcg(src4 + i);
+  }
   const T *in = (const T *)P.logits + (size_t)row * P.ld_in;
   T *out = (T *)P.out + (size_t)row * P.ld_out;
   const bool inplace = (P.flags & QRITA_INPLACE) != 0;
@@ -1310,6 +1319,16 @@ __global__ void __launch_bounds__(kThreads, 2) qrita_tail(Params P) {
   }
 }
 
+template <typename T, int NP>
+__global__ void __launch_bounds__(kThreads, 1) qrita_tail(Params P) {
+  extern __shared__ __align__(16) uint8_t dsmem[];
+  __shared__ TailSmem sm;
+  __shared__ uint32_t s_off[kMaxTailChunks + 1];
+  __shared__ uint32_t s_part[2][kWarps][5];
+  tail_body<T, NP>(P, dsmem, sm, s_off, s_part);
+  pdl_wait();  // complete only after the whole streaming grid has (stream-order guarantee)
+}
+
 // ------------------------------------------------------------------------------------------------
 // K1: streaming pass + row tails
 // ------------------------------------------------------------------------------------------------
@@ -1491,7 +1510,11 @@ __global__ void __launch_bounds__(kStreamThreads, 3) qrita_stream(Params P) {
       cs.maxkey = mx; cs.count = base; cs.nf_col = nf; cs.minkey = mn;
       P.cstats[item] = cs;
     }
+    // publish: outliers, statistics and the -inf background of this chunk are visible before the
+    // row counter moves (the row tail polls it)
+    __threadfence();
     __syncwarp();
+    if (lane == 0) atomicAdd(P.row_done + row, 1u);
   }
   if (!waited) pdl_wait();
 }
@@ -1499,7 +1522,8 @@ __global__ void __launch_bounds__(kStreamThreads, 3) qrita_stream(Params P) {
 constexpr size_t kTailDynSmem = (size_t)kCapX * 8 + (size_t)kCapS * 16 + (size_t)kCapA * 12;
 
 template <typename T, int NP, bool VEC>
-static cudaError_t launch_pipeline(const Params &P, cudaStream_t st, cudaEvent_t prep_done) {
+static cudaError_t launch_pipeline(const Params &P, cudaStream_t st, cudaEvent_t prep_done,
+                                   cudaEvent_t stream_done) {
   static int stream_grid = 0;  // per instantiation
   if (stream_grid == 0) {
     cudaError_t e = cudaFuncSetAttribute(qrita_tail<T, NP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1510,7 +1534,11 @@ static cudaError_t launch_pipeline(const Params &P, cudaStream_t st, cudaEvent_t
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, qrita_stream<T, VEC>, kStreamThreads, 0);
     if (e != cudaSuccess) return e;
-    stream_grid = sms * (per_sm < 1 ? 1 : per_sm);
+    // two streaming CTAs per SM leave room for one row-tail CTA, so tails run while rows stream
+    int want = 3;
+    if (const char *ev = getenv("QRITA_STREAM_CTAS_PER_SM")) want = atoi(ev);
+    if (want < 1) want = 1;
+    stream_grid = sms * (per_sm < want ? (per_sm < 1 ? 1 : per_sm) : want);
   }
   qrita_prep<T><<<P.B, 256, 0, st>>>(P);
   cudaError_t e = cudaGetLastError();
@@ -1534,7 +1562,11 @@ static cudaError_t launch_pipeline(const Params &P, cudaStream_t st, cudaEvent_t
   cfg.numAttrs = 1;
   e = cudaLaunchKernelEx(&cfg, qrita_stream<T, VEC>, P);
   if (e != cudaSuccess) return e;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  if (stream_done) {
+    e = cudaEventRecord(stream_done, st);
+    if (e != cudaSuccess) return e;
+  }
+  attr[0].val.programmaticStreamSerializationAllowed = stream_done ? 0 : 1;
   cfg.gridDim = dim3((unsigned)P.B);
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = kTailDynSmem;
@@ -1542,10 +1574,13 @@ static cudaError_t launch_pipeline(const Params &P, cudaStream_t st, cudaEvent_t
 }
 
 template <typename T>
-static cudaError_t launch_all(const Params &P, cudaStream_t st, bool vec, cudaEvent_t prep_done) {
+static cudaError_t launch_all(const Params &P, cudaStream_t st, bool vec, cudaEvent_t prep_done,
+                              cudaEvent_t stream_done) {
   if (P.flags & QRITA_SEARCH_BINARY)
-    return vec ? launch_pipeline<T, 1, true>(P, st, prep_done) : launch_pipeline<T, 1, false>(P, st, prep_done);
-  return vec ? launch_pipeline<T, 3, true>(P, st, prep_done) : launch_pipeline<T, 3, false>(P, st, prep_done);
+    return vec ? launch_pipeline<T, 1, true>(P, st, prep_done, stream_done)
+               : launch_pipeline<T, 1, false>(P, st, prep_done, stream_done);
+  return vec ? launch_pipeline<T, 3, true>(P, st, prep_done, stream_done)
+             : launch_pipeline<T, 3, false>(P, st, prep_done, stream_done);
 }
 
 }  // namespace qrita

@@ -29,7 +29,7 @@ enum Status : int32_t { ST_BAD_K = 1, ST_BAD_P = 2, ST_NONFINITE = 4 };
 // ------------------------------------------------------------------------------------------------
 // Workspace records
 // ------------------------------------------------------------------------------------------------
-struct RowPlan {
+struct alignas(16) RowPlan {
   uint32_t key_thr;   // outlier iff key >= key_thr
   int32_t mode;
   int64_t k;
@@ -38,8 +38,9 @@ struct RowPlan {
   Fx t_p;             // smallest exact mass whose fsum is >= p
   Fx t_sp;            // smallest exact mass whose fsum is >= succ(p), i.e. > p
   int32_t has_thr;    // 0: no outliers gathered for this row
-  int32_t pad;
+  int32_t pad[3];
 };
+static_assert(sizeof(RowPlan) % 16 == 0, "RowPlan is copied with 16-byte loads");
 
 struct ChunkStat {
   uint32_t maxkey;
@@ -81,6 +82,7 @@ struct Params {
   int32_t *status;
   int32_t *nf_col;
   unsigned long long *dbg;  // [B][16] phase timestamps of the row tail (QRITA_DEBUG_TIMING)
+  uint32_t *row_done;       // [B] chunks of the row finished by qrita_stream (zeroed by qrita_prep)
   int nchunks;
   int total_items;
   PwTree tree;
@@ -90,7 +92,7 @@ struct Params {
 // rewritten by each call (no state carries over), and the status block only depends on B, so
 // qrita_get_status needs no V.
 struct WsLayout {
-  size_t status, nf_col, dbg, plans, cstats, cand_bits, cand_idx, total;
+  size_t status, nf_col, dbg, row_done, plans, cstats, cand_bits, cand_idx, total;
 };
 
 inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
@@ -102,6 +104,7 @@ inline WsLayout ws_layout(int B, int V) {
   L.status = off;    off = align_up(off + 4ull * (size_t)B, 256);
   L.nf_col = off;    off = align_up(off + 4ull * (size_t)B, 256);
   L.dbg = off;       off = align_up(off + 128ull * (size_t)B, 256);
+  L.row_done = off;  off = align_up(off + 4ull * (size_t)B, 256);
   L.plans = off;     off = align_up(off + sizeof(RowPlan) * (size_t)B, 256);
   L.cstats = off;    off = align_up(off + sizeof(ChunkStat) * (size_t)B * nchunks, 256);
   L.cand_bits = off; off = align_up(off + 4ull * (size_t)B * nchunks * kCapChunk, 256);
@@ -111,7 +114,9 @@ inline WsLayout ws_layout(int B, int V) {
 }
 
 
-cudaError_t launch_f32(const Params &P, cudaStream_t st, bool vec, cudaEvent_t prep_done);
-cudaError_t launch_bf16(const Params &P, cudaStream_t st, bool vec, cudaEvent_t prep_done);
+cudaError_t launch_f32(const Params &P, cudaStream_t st, bool vec, cudaEvent_t prep_done,
+                       cudaEvent_t stream_done);
+cudaError_t launch_bf16(const Params &P, cudaStream_t st, bool vec, cudaEvent_t prep_done,
+                        cudaEvent_t stream_done);
 
 }  // namespace qrita

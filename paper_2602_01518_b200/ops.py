@@ -143,14 +143,16 @@ def topk_topp(logits: torch.Tensor, k: Union[int, torch.Tensor], p: Union[float,
               flags: Optional[TruncFlags] = None, sample_size: int = DEFAULT_SAMPLE_SIZE,
               kept_count: Optional[torch.Tensor] = None, metrics: Optional[torch.Tensor] = None,
               check: bool = True, stream: Optional[torch.cuda.Stream] = None,
-              prep_event: Optional[torch.cuda.Event] = None) -> torch.Tensor:
+              prep_event: Optional[torch.cuda.Event] = None,
+              stream_event: Optional[torch.cuda.Event] = None) -> torch.Tensor:
     """Exact Top-k then Top-p truncation of a [B, V] CUDA tensor (fp32 or bf16).
 
     k: int64 per row (k == V disables top-k); p: float64 per row (p == 1 disables top-p).  Returns
     the masked logits (new tensor, or `logits` itself when inplace).  kept_count (int32 [B]) and
     metrics (uint8 [B, 40], qrita_row_metrics) are filled when given.  check=True synchronises and
     raises the reference's ValueError for invalid rows; check=False leaves the call fully async.
-    prep_event (profiling) is recorded between the preparation and the streaming kernel.
+    prep_event / stream_event (profiling only) are recorded after the preparation / streaming kernel;
+    either one serialises the launches around it so the kernels can be timed alone.
     """
     if not isinstance(logits, torch.Tensor) or not logits.is_cuda:
         raise TypeError("logits must be a CUDA tensor (there is no CPU path)")
@@ -181,10 +183,13 @@ def topk_topp(logits: torch.Tensor, k: Union[int, torch.Tensor], p: Union[float,
     ws = workspace_for(dev, st)
     with torch.cuda.device(dev):
         ws_ptr, ws_bytes = ws.get(need, st)
-        ev = 0
+        ev = ev2 = 0
         if prep_event is not None:
             prep_event.record(st)  # materialise the event handle, re-recorded by the library
             ev = prep_event.cuda_event
+        if stream_event is not None:
+            stream_event.record(st)
+            ev2 = stream_event.cuda_event
         rc = lib.qrita_topk_topp_ex(
             ctypes.c_void_p(logits.data_ptr()), _row_stride(logits), _DTYPES[logits.dtype], b, v,
             ctypes.c_void_p(kt.data_ptr()), ctypes.c_void_p(pt.data_ptr()),
@@ -192,7 +197,7 @@ def topk_topp(logits: torch.Tensor, k: Union[int, torch.Tensor], p: Union[float,
             ctypes.c_void_p(kept_count.data_ptr() if kept_count is not None else 0),
             ctypes.c_void_p(metrics.data_ptr() if metrics is not None else 0),
             ctypes.c_void_p(ws_ptr), ws_bytes, fl, int(sample_size),
-            ctypes.c_void_p(st.cuda_stream), ctypes.c_void_p(ev))
+            ctypes.c_void_p(st.cuda_stream), ctypes.c_void_p(ev), ctypes.c_void_p(ev2))
         if rc != N.OK:
             ws.reset()
             raise RuntimeError(f"qrita_topk_topp failed: {N.strerror(rc)}")
