@@ -988,12 +988,7 @@ template <typename T, int NP>
 __device__ __forceinline__ void tail_body(const Params &P, uint8_t *dsmem, TailSmem &sm, uint32_t *s_off,
                                           uint32_t (*s_part)[kWarps][5]) {
   const int row = blockIdx.x;
-  // Runs concurrently with qrita_stream (programmatic launch): wait for this row's chunks only.
-  if (threadIdx.x == 0) {
-    const uint32_t need = (uint32_t)P.nchunks;
-    while (ld_acquire_gpu(P.row_done + row) < need) __nanosleep(256);
-  }
-  __syncthreads();
+  pdl_wait();  // outliers and chunk statistics of qrita_stream (and plans of qrita_prep)
   const bool dbg = (P.flags & QRITA_DEBUG_TIMING) != 0;
 #define QRITA_TSTAMP(i)                                                                 \
   do {                                                                                  \
@@ -1320,13 +1315,12 @@ __device__ __forceinline__ void tail_body(const Params &P, uint8_t *dsmem, TailS
 }
 
 template <typename T, int NP>
-__global__ void __launch_bounds__(kThreads, 1) qrita_tail(Params P) {
+__global__ void __launch_bounds__(kThreads, 2) qrita_tail(Params P) {
   extern __shared__ __align__(16) uint8_t dsmem[];
   __shared__ TailSmem sm;
   __shared__ uint32_t s_off[kMaxTailChunks + 1];
   __shared__ uint32_t s_part[2][kWarps][5];
   tail_body<T, NP>(P, dsmem, sm, s_off, s_part);
-  pdl_wait();  // complete only after the whole streaming grid has (stream-order guarantee)
 }
 
 // ------------------------------------------------------------------------------------------------
@@ -1510,11 +1504,7 @@ __global__ void __launch_bounds__(kStreamThreads, 3) qrita_stream(Params P) {
       cs.maxkey = mx; cs.count = base; cs.nf_col = nf; cs.minkey = mn;
       P.cstats[item] = cs;
     }
-    // publish: outliers, statistics and the -inf background of this chunk are visible before the
-    // row counter moves (the row tail polls it)
-    __threadfence();
     __syncwarp();
-    if (lane == 0) atomicAdd(P.row_done + row, 1u);
   }
   if (!waited) pdl_wait();
 }

@@ -70,6 +70,35 @@ if len(sys.argv) > 1 and sys.argv[1] == "stats":
             vals = [r[f] for r in m]
             print(f"{cfg} {f}: mean {st.mean(vals):.2f} max {max(vals)}")
 
+if len(sys.argv) > 1 and sys.argv[1] == "wtiming":
+    import bench, ctypes
+    from paper_2602_01518_b200 import _native as N
+    for cfg in sys.argv[2:]:
+        x, k, p, dtype, desc = bench.workload(cfg)
+        xt = torch.from_numpy(x).cuda()
+        kt, pt = torch.from_numpy(k).cuda(), torch.from_numpy(p).cuda()
+        fl = Q.TruncFlags(debug_timing=True)
+        for _ in range(3):
+            Q.topk_topp(xt, kt, pt, flags=fl)
+        torch.cuda.synchronize()
+        st = torch.cuda.current_stream()
+        ws = Q.ops.workspace_for(xt.device, st)
+        ptr, _ = ws.get(0, st)
+        B = x.shape[0]
+        buf = (ctypes.c_ulonglong * (16 * B))()
+        N.load().qrita_get_timing(ctypes.c_void_p(ptr), B, buf, ctypes.c_void_p(st.cuda_stream))
+        a = np.frombuffer(buf, dtype=np.uint64).reshape(B, 16).astype(np.int64)
+        t0 = a[:, 0]
+        print(f"{cfg}: row completion spread {(t0.max()-t0.min())/1e3:.1f} us; last tail end {(a[:,9].max()-t0.min())/1e3:.1f} us")
+        names = ["lock", "stats", "stage", "kbracket", "kpivot", "S+D+pi", "pbracket", "ppivot", "scatter"]
+        prev = a[:, 0]
+        for i, nm in enumerate(names, start=1):
+            cur = a[:, i]
+            ok = cur > 0
+            d = np.where(ok, cur - prev, 0)
+            print(f"   {nm:9s} mean {d[ok].mean()/1e3 if ok.any() else 0:8.2f} us  max {d.max()/1e3:8.2f}")
+            prev = np.where(ok, cur, prev)
+
 if len(sys.argv) > 1 and sys.argv[1] == "timing":
     import bench, ctypes
     from paper_2602_01518_b200 import _native as N
