@@ -340,7 +340,7 @@ def main():
         line["e2e"] = {"value": e2e_val, "unit": "rows/s", "h2d_bytes_per_step": h2d,
                        "d2h_bytes_per_step": d2h, "ms_per_step": statistics.mean(tt)}
         if rank == 0 and world == 1 and not args.no_cpu_baseline:
-            rows = min(b, 64)
+            rows = b
             procs = min(os.cpu_count() or 1, rows)
             val, wall = cpu_baseline_oracle(x_np, k_np, p_np, rows, procs)
             line["cpu_baseline"] = {"value": val, "unit": "rows/s", "cores": procs, "kind": "port",
