@@ -41,6 +41,9 @@ def workload(name: str, rank: int = 0):
         r = np.random.default_rng(42 + rank)
         return x, r.integers(1, 1025, 256).astype(np.int64), r.uniform(0.5, 0.99, 256), "f32", \
             "cfg2: Llama-3 V=128256, B=256 fp32, k~U{1..1024}, p~U[0.5,0.99]"
+    if name == "cfg2h":  # first 128 rows of cfg2 (one row tail per SM)
+        x, k, p, dt, _ = workload("cfg2")
+        return x[:128].copy(), k[:128].copy(), p[:128].copy(), dt, "cfg2 rows 0-127"
     if name == "cfg2copy":  # streaming floor: same matrix, k = V and p = 1 (passthrough copy)
         x = np.random.default_rng(1).normal(0.0, 1.0, (256, 128256)).astype(np.float32)
         return x, np.full(256, 128256, np.int64), np.full(256, 1.0), "f32", "cfg2 matrix, passthrough"

@@ -176,6 +176,22 @@ __device__ __forceinline__ Fx fx_round_threshold(double p) {
 }
 
 // ------------------------------------------------------------------------------------------------
+// L2 cache policies
+// ------------------------------------------------------------------------------------------------
+__device__ __forceinline__ unsigned long long l2_evict_last_policy() {
+  unsigned long long pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ void st_keep_u32(uint32_t *p, uint32_t v, unsigned long long pol) {
+  asm volatile("st.global.L2::cache_hint.b32 [%0], %1, %2;" :: "l"(p), "r"(v), "l"(pol) : "memory");
+}
+__device__ __forceinline__ void st_keep_u4(uint4 *p, uint4 v, unsigned long long pol) {
+  asm volatile("st.global.L2::cache_hint.v4.b32 [%0], {%1, %2, %3, %4}, %5;"
+               :: "l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w), "l"(pol) : "memory");
+}
+
+// ------------------------------------------------------------------------------------------------
 // Programmatic dependent launch (griddepcontrol, sm_90+)
 // ------------------------------------------------------------------------------------------------
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }

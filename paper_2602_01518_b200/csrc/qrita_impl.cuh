@@ -1395,6 +1395,7 @@ __global__ void __launch_bounds__(kStreamThreads, 3) qrita_stream(Params P) {
   const bool inplace = (P.flags & QRITA_INPLACE) != 0;
   const uint32_t lt = (1u << lane) - 1u;
   const float qnan = __uint_as_float(0x7fffffffu);
+  const unsigned long long keep_pol = l2_evict_last_policy();
   bool waited = false;
 
   for (int item = gwarp; item < P.total_items; item += nwarps) {
@@ -1495,15 +1496,13 @@ __global__ void __launch_bounds__(kStreamThreads, 3) qrita_stream(Params P) {
     __syncwarp();
     const size_t slot = (size_t)item * kCapChunk;
     const uint32_t nst = base < (uint32_t)kCapChunk ? base : (uint32_t)kCapChunk;
+    // outliers and statistics are re-read by the row tail: keep them in L2 (evict_last) while the
+    // logits stream past with evict_first
     for (uint32_t j = lane; j < nst; j += 32) {
-      P.cand_bits[slot + j] = s_cb[wib][j];
-      P.cand_idx[slot + j] = s_ci[wib][j];
+      st_keep_u32(P.cand_bits + slot + j, s_cb[wib][j], keep_pol);
+      st_keep_u32(P.cand_idx + slot + j, s_ci[wib][j], keep_pol);
     }
-    if (lane == 0) {
-      ChunkStat cs;
-      cs.maxkey = mx; cs.count = base; cs.nf_col = nf; cs.minkey = mn;
-      P.cstats[item] = cs;
-    }
+    if (lane == 0) st_keep_u4(reinterpret_cast<uint4 *>(P.cstats + item), make_uint4(mx, base, nf, mn), keep_pol);
     __syncwarp();
   }
   if (!waited) pdl_wait();
