@@ -120,14 +120,14 @@ int qrita_topk_topp_ex(const void *logits, int64_t ld_in, int dtype, int B, int 
   P.B = B; P.V = V; P.dtype = dtype; P.flags = flags; P.sample_size = sample_size;
   P.k = k; P.p = p; P.kept_count = kept_count; P.metrics = metrics;
   P.plans = (RowPlan *)(ws + L.plans);
-  P.cstats = (ChunkStat *)(ws + L.cstats);
+  P.agg = (RowAgg *)(ws + L.agg);
   P.cand_bits = (uint32_t *)(ws + L.cand_bits);
   P.cand_idx = (uint32_t *)(ws + L.cand_idx);
   P.status = (int32_t *)(ws + L.status);
   P.nf_col = (int32_t *)(ws + L.nf_col);
   P.dbg = (unsigned long long *)(ws + L.dbg);
-  P.row_done = (uint32_t *)(ws + L.row_done);
   P.nchunks = (int)nchunks;
+  P.xcap = row_cap(V);
   P.total_items = (int)((size_t)B * nchunks);
   pw_tree(sample_size < V ? sample_size : V, P.tree);
 

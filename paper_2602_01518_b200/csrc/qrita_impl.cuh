@@ -314,7 +314,9 @@ __global__ void __launch_bounds__(256) qrita_prep(Params P) {
     P.plans[row] = pl;
     P.status[row] = (bad_k ? ST_BAD_K : 0) | (bad_p ? ST_BAD_P : 0);
     P.nf_col[row] = -1;
-    P.row_done[row] = 0u;
+    uint4 *ag = reinterpret_cast<uint4 *>(P.agg + row);
+    ag[0] = make_uint4(0u, 0u, 0xffffffffu, 0xffffffffu);  // count, maxkey, minkey, nf_col
+    ag[1] = make_uint4(0u, 0u, 0u, 0u);                     // ovf, done
   }
 }
 
@@ -336,8 +338,65 @@ struct TailSmem {
   uint32_t u[8];                // broadcast scalars
   uint32_t ctot[kWarps];        // bracket pass: per-warp count totals
   Fx mtot[kWarps];              // bracket pass: per-warp mass totals
+  uint32_t scan_u[kWarps];      // bin sort: warp totals of the bin-start scan
+  Fx scan_f[2][kWarps];         // bin sort: warp totals of the two mass scans
+  uint32_t bstar, nabove, bail, L;
   SearchState st;
 };
+
+// ------------------------------------------------------------------------------------------------
+// Block scans (one value per thread, thread order); each buffer is reused only after a barrier
+// ------------------------------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t block_exscan_u32(uint32_t v, uint32_t *buf, uint32_t &total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t incl = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t u = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += u;
+  }
+  if (lane == 31) buf[warp] = incl;
+  __syncthreads();
+  uint32_t before = 0u, tot = 0u;
+#pragma unroll
+  for (int w = 0; w < kWarps; ++w) {
+    const uint32_t t = buf[w];
+    before += (w < warp) ? t : 0u;
+    tot += t;
+  }
+  total = tot;
+  return before + incl - v;
+}
+
+__device__ __forceinline__ Fx block_exscan_fx(const Fx &v, Fx *buf, Fx &total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  Fx incl = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    Fx u;
+    u.w0 = __shfl_up_sync(0xffffffffu, incl.w0, o);
+    u.w1 = __shfl_up_sync(0xffffffffu, incl.w1, o);
+    u.w2 = __shfl_up_sync(0xffffffffu, incl.w2, o);
+    if (lane >= o) incl = fx_add(incl, u);
+  }
+  if (lane == 31) buf[warp] = incl;
+  __syncthreads();
+  Fx before = fx_zero(), tot = fx_zero();
+#pragma unroll
+  for (int w = 0; w < kWarps; ++w) {
+    const Fx t = buf[w];
+    if (w < warp) before = fx_add(before, t);
+    tot = fx_add(tot, t);
+  }
+  total = tot;
+  return fx_sub(fx_add(before, incl), v);
+}
+
+// Smallest s with w <= kNB * 2^s: key bins (l, l + 2^s], (l + 2^s, l + 2^(s+1)], ... cover (l, l + w].
+__device__ __forceinline__ int bin_shift(uint32_t w) {
+  if (w <= (uint32_t)kNB) return 0;
+  return (32 - __clz(w - 1u)) - kLogNB;
+}
 
 constexpr int kBins = 256;  // buckets of the bracketing pass (== kThreads: one bucket per thread)
 
@@ -985,8 +1044,7 @@ __device__ void write_row(const T *in, T *out, int V, uint32_t K, uint32_t cut, 
 }
 
 template <typename T, int NP>
-__device__ __forceinline__ void tail_body(const Params &P, uint8_t *dsmem, TailSmem &sm, uint32_t *s_off,
-                                          uint32_t (*s_part)[kWarps][5]) {
+__device__ __forceinline__ void tail_body(const Params &P, uint8_t *dsmem, TailSmem &sm) {
   const int row = blockIdx.x;
   pdl_wait();  // outliers and chunk statistics of qrita_stream (and plans of qrita_prep)
   const bool dbg = (P.flags & QRITA_DEBUG_TIMING) != 0;
@@ -1001,7 +1059,6 @@ __device__ __forceinline__ void tail_body(const Params &P, uint8_t *dsmem, TailS
   QRITA_TSTAMP(0);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int V = P.V;
-  const int nch = P.nchunks;
   RowPlan pl;
   {
     const uint4 *src4 = reinterpret_cast<const uint4 *>(P.plans + row);
@@ -1022,44 +1079,32 @@ __device__ __forceinline__ void tail_body(const Params &P, uint8_t *dsmem, TailS
   double *sp = (double *)(si + kCapS);   // [kCapS] survivor exp / probability
   double *ap = sp + kCapS;               // [kCapA] active-set probabilities (top-p search)
   uint32_t *ak = (uint32_t *)(ap + kCapA);  // [kCapA] active-set keys (3*kCapA keys for top-k)
+  // bin-sort layout of the same work area
+  uint32_t *hc = sb;                     // [kNB] outliers per key bin
+  uint32_t *he = hc + kNB;               // [kNB] bin starts (descending order) -> cursors -> ends
+  uint32_t *cb = he + kNB;               // [kCapC] candidates grouped by bin: bits
+  uint32_t *ci = cb + kCapC;             //                                     indices
+  uint32_t *db = ci + kCapC;             // [kCapC] candidates sorted (key desc, index asc): bits
+  uint32_t *di = db + kCapC;             //                                                  indices
+  double *ev = (double *)cb;             // [kCapC] survivor exp values (after the sort)
+  for (int i = tid; i < kNB; i += kThreads) hc[i] = 0u;
 
-  // ---- per-row totals and per-chunk outlier offsets (block scan over the chunk statistics)
-  uint32_t maxkey = 0u, minkey = 0xffffffffu, n_c = 0u, nf_col = 0xffffffffu, ovf = 0u;
-  for (int t0 = 0, par = 0; t0 < nch; t0 += kThreads, par ^= 1) {
-    const int c = t0 + tid;
-    uint4 q = make_uint4(0u, 0u, 0xffffffffu, 0xffffffffu);
-    if (c < nch) q = __ldcg(reinterpret_cast<const uint4 *>(P.cstats + (size_t)row * nch + c));
-    const uint32_t cc = q.y;
-    uint32_t incl = cc;
+  // ---- one round trip: the row aggregate, and speculatively the first kSpecTail * kThreads
+  // outliers of the row buffer (coalesced; entries past the count are ignored)
+  const size_t rb = (size_t)row * P.xcap;
+  const uint4 a0 = __ldcg(reinterpret_cast<const uint4 *>(P.agg + row));
+  const uint4 a1 = __ldcg(reinterpret_cast<const uint4 *>(P.agg + row) + 1);
+  uint32_t vb[kSpecTail], vi[kSpecTail];
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += v;
-    }
-    if (lane == 31) s_part[par][warp][0] = incl;
-    const uint32_t wmx = warp_max(c < nch ? q.x : 0u), wmn = warp_min(q.w), wnf = warp_min(q.z);
-    const uint32_t wov = warp_max(cc > (uint32_t)kCapChunk ? 1u : 0u);
-    if (lane == 0) { s_part[par][warp][1] = wmx; s_part[par][warp][2] = wmn; s_part[par][warp][3] = wnf;
-                     s_part[par][warp][4] = wov; }
-    __syncthreads();
-    uint32_t before = 0u, tile = 0u;
-#pragma unroll
-    for (int w = 0; w < kWarps; ++w) {
-      const uint32_t tw = s_part[par][w][0];
-      before += (w < warp) ? tw : 0u;
-      tile += tw;
-      maxkey = max(maxkey, s_part[par][w][1]);
-      minkey = min(minkey, s_part[par][w][2]);
-      nf_col = min(nf_col, s_part[par][w][3]);
-      ovf |= s_part[par][w][4];
-    }
-    if (c < nch && c < kMaxTailChunks) s_off[c] = n_c + before + incl - cc;
-    n_c += tile;
+  for (int j = 0; j < kSpecTail; ++j) {
+    const int i = tid + j * kThreads;
+    vb[j] = vi[j] = 0u;
+    if (i < P.xcap) { vb[j] = __ldcg(P.cand_bits + rb + i); vi[j] = __ldcg(P.cand_idx + rb + i); }
   }
-  if (tid == 0 && nch <= kMaxTailChunks) s_off[nch] = n_c;
-  const bool overflow = ovf != 0u || nch > kMaxTailChunks;
+  const uint32_t n_c = a0.x, maxkey = a0.y, minkey = a0.z, nf_col = a0.w;
+  const bool overflow = a1.x != 0u || n_c > (uint32_t)P.xcap;
   const uint32_t lo_row = minkey ? minkey - 1u : 0u;  // below every key of the row
-  __syncthreads();
+  __syncthreads();  // bin counters zeroed
   QRITA_TSTAMP(1);
 
   qrita_row_metrics met;
@@ -1093,38 +1138,157 @@ __device__ __forceinline__ void tail_body(const Params &P, uint8_t *dsmem, TailS
   const double m = value_of_key(maxkey);
   met.outlier_count = sigma ? (int32_t)n_c : 0;
 
-  // ---- stage the outliers in shared memory (index order) when they fit
+  // ---- stage the outliers in shared memory when they fit
   const bool x_fits = sigma && !overflow && n_c <= (uint32_t)kCapX;
+  // bin-sort resolve: sigma hit (count > k, sigma_trunc.py:127-133) of a top-k / top-k+top-p row
+  const bool bins = x_fits && NP == 3 && !force_fb && !nodup && (mode == MODE_TOPK || mode == MODE_TOPKP) &&
+                    pl.k <= (int64_t)kCapC && n_c > (uint32_t)pl.k;
+  const uint32_t bl = pl.key_thr ? pl.key_thr - 1u : 0u;  // every outlier key is > bl
+  const int bsh = bin_shift(maxkey - bl);
   if (x_fits) {
-    // one thread per chunk: 16-byte loads straight from the chunk's slots (slots are 1 KB aligned),
-    // all issued before the shared-memory stores
-    for (int c = tid; c < nch; c += kThreads) {
-      const uint32_t off = s_off[c], cc = s_off[c + 1] - off;
-      const size_t slot = ((size_t)row * nch + c) * kCapChunk;
-      const uint4 *pb = reinterpret_cast<const uint4 *>(P.cand_bits + slot);
-      const uint4 *pi = reinterpret_cast<const uint4 *>(P.cand_idx + slot);
-      for (uint32_t j0 = 0; j0 < cc; j0 += 32u) {
-        uint4 qb[8], qi[8];
+    // outliers in chunk-completion order (each chunk's run is in index order); bins counted on the way
 #pragma unroll
-        for (int g = 0; g < 8; ++g) {
-          if (j0 + 4u * g < cc) { qb[g] = __ldcg(pb + (j0 >> 2) + g); qi[g] = __ldcg(pi + (j0 >> 2) + g); }
-        }
+    for (int j = 0; j < kSpecTail; ++j) {
+      const uint32_t i = (uint32_t)(tid + j * kThreads);
+      if (i < n_c) {
+        xb[i] = vb[j]; xi[i] = vi[j];
+        if (bins) atomicAdd(&hc[(key_of_bits(vb[j]) - bl - 1u) >> bsh], 1u);
+      }
+    }
+    for (uint32_t i0 = kSpecTail * kThreads; i0 < n_c; i0 += 4 * kThreads) {
+      uint32_t b4[4], x4[4];
 #pragma unroll
-        for (int g = 0; g < 8; ++g) {
-          const uint32_t j = j0 + 4u * g;
-          if (j < cc) {
-            const uint32_t vb[4] = {qb[g].x, qb[g].y, qb[g].z, qb[g].w};
-            const uint32_t vi[4] = {qi[g].x, qi[g].y, qi[g].z, qi[g].w};
+      for (int j = 0; j < 4; ++j) {
+        const uint32_t i = i0 + tid + j * kThreads;
+        b4[j] = x4[j] = 0u;
+        if (i < n_c) { b4[j] = __ldcg(P.cand_bits + rb + i); x4[j] = __ldcg(P.cand_idx + rb + i); }
+      }
 #pragma unroll
-            for (int e = 0; e < 4; ++e)
-              if (j + e < cc) { xb[off + j + e] = vb[e]; xi[off + j + e] = vi[e]; }
-          }
+      for (int j = 0; j < 4; ++j) {
+        const uint32_t i = i0 + tid + j * kThreads;
+        if (i < n_c) {
+          xb[i] = b4[j]; xi[i] = x4[j];
+          if (bins) atomicAdd(&hc[(key_of_bits(b4[j]) - bl - 1u) >> bsh], 1u);
         }
       }
     }
     __syncthreads();
   }
   QRITA_TSTAMP(2);
+
+  uint32_t Kf = 0u, cutf = kNoCut, kept = (uint32_t)V;
+  bool k_used_x = false;  // the final kept set is a subset of X
+  bool full_row = false;
+  bool sorted_out = false;  // the kept set is db/di[0, kept) (bin-sort resolve)
+
+  // ================= bin-sort resolve (pipeline.py:199-239 on a sigma hit) =================
+  // The kept set of the oracle (oracle.py:70-89) is a prefix of the (value desc, index asc) order, so
+  // sort the few candidates that can be in it and take prefixes: top-k is the first k, top-p the
+  // shortest prefix of the top-k whose exactly-summed renormalised mass reaches p.
+  if (bins) {
+    const uint32_t k = (uint32_t)pl.k;
+    // 1. bin starts in descending order; the bin holding the k-th largest key
+    uint32_t c4[4], loc = 0u;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) { c4[j] = hc[kNB - 1 - 4 * tid - j]; loc += c4[j]; }
+    uint32_t tot;
+    uint32_t run = block_exscan_u32(loc, sm.scan_u, tot);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int b = kNB - 1 - 4 * tid - j;
+      he[b] = run;
+      if (run < k && k <= run + c4[j]) { sm.bstar = (uint32_t)b; sm.nabove = run; }
+      run += c4[j];
+    }
+    if (tid == 0) { sm.bail = 0u; sm.L = k; }
+    __syncthreads();
+    QRITA_TSTAMP(10);
+    const uint32_t bstar = sm.bstar;
+    const uint32_t nC = sm.nabove + hc[bstar];
+    if (nC <= (uint32_t)kCapC) {  // block-uniform
+      // 2. counting sort by bin (bins >= b*); order inside a bin is arbitrary so far
+      for (int i = tid; i < (int)n_c; i += kThreads) {
+        const uint32_t b = xb[i];
+        const uint32_t bin = (key_of_bits(b) - bl - 1u) >> bsh;
+        if (bin >= bstar) {
+          const uint32_t pos = atomicAdd(&he[bin], 1u);
+          cb[pos] = b; ci[pos] = xi[i];
+        }
+      }
+      __syncthreads();
+      QRITA_TSTAMP(11);
+      // 3. order inside every bin by (key desc, index asc): rank against the bin's other entries
+      for (int q = tid; q < (int)nC; q += kThreads) {
+        const uint32_t b = cb[q], ix = ci[q], key = key_of_bits(b);
+        const uint32_t bin = (key - bl - 1u) >> bsh;
+        const uint32_t e = he[bin], c = hc[bin];
+        if (c > (uint32_t)kMaxBin) { sm.bail = 1u; continue; }
+        uint32_t r = 0u;
+        for (uint32_t j = e - c; j < e; ++j) {
+          const uint32_t kj = key_of_bits(cb[j]);
+          r += (kj > key || (kj == key && ci[j] < ix)) ? 1u : 0u;
+        }
+        db[e - c + r] = b; di[e - c + r] = ix;
+      }
+      __syncthreads();
+      QRITA_TSTAMP(12);
+      if (sm.bail == 0u) {  // block-uniform
+        uint32_t L = k;
+        if (mode == MODE_TOPKP) {
+          // 4. normaliser over the k survivors (oracle.py:85-86): exact sum, rounded once
+          const int E = ((int)k + kThreads - 1) / kThreads;
+          const int q0 = tid * E;
+          Fx se = fx_zero();
+          for (int j = 0; j < E; ++j) {
+            const int q = q0 + j;
+            if (q < (int)k) {
+              const double e = exp((double)__uint_as_float(db[q]) - m);
+              ev[q] = e;
+              se = fx_add(se, fx_from_double(e));
+            }
+          }
+          Fx Dx;
+          (void)block_exscan_fx(se, sm.scan_f[0], Dx);
+          const double D = fx_to_double(Dx);
+          QRITA_TSTAMP(13);
+          // 5. exact prefix masses in sorted order; the first prefix whose fsum reaches p
+          Fx sp_loc = fx_zero();
+          for (int j = 0; j < E; ++j) {
+            const int q = q0 + j;
+            if (q < (int)k) {
+              const double pi = ev[q] / D;
+              ev[q] = pi;
+              sp_loc = fx_add(sp_loc, fx_from_double(pi));
+            }
+          }
+          Fx Mtot;
+          Fx pre = block_exscan_fx(sp_loc, sm.scan_f[1], Mtot);
+          QRITA_TSTAMP(14);
+          for (int j = 0; j < E; ++j) {
+            const int q = q0 + j;
+            if (q < (int)k) {
+              pre = fx_add(pre, fx_from_double(ev[q]));
+              if (fx_ge(pre, pl.t_p)) { atomicMin(&sm.L, (uint32_t)q + 1u); break; }
+            }
+          }
+          __syncthreads();
+          // p >= fsum(all survivors): keep them all (oracle.py:45-46)
+          L = fx_ge(Mtot, pl.t_sp) ? sm.L : k;
+          met.p_search_iters = 1;
+        }
+        met.k_search_iters = 1;
+        met.trunc_hit = 1;
+        met.fallback_used = 0;
+        Kf = key_of_bits(db[L - 1u]);
+        cutf = di[L - 1u];
+        kept = L;
+        k_used_x = true;
+        sorted_out = true;
+      }
+    }
+    __syncthreads();
+  }
+  QRITA_TSTAMP(3);
   const SrcX X{xb, xi, (int)n_c};
   const SrcRow<T> RW{in, V};
   Red red(sm);
@@ -1135,13 +1299,9 @@ __device__ __forceinline__ void tail_body(const Params &P, uint8_t *dsmem, TailS
   red.hms = (unsigned long long *)ap;               // 5 * kBins * 8 B = 10 KB
   red.hcnt = (uint32_t *)(red.hms + 5 * kBins);     // + 1 KB  (region: 12 KB)
 
-  uint32_t Kf = 0u, cutf = kNoCut, kept = (uint32_t)V;
-  bool k_used_x = false;  // the final kept set is a subset of X
-  bool full_row = false;
-
   // ================= top-k stage: _topk_plan, pipeline.py:88-119 =================
   uint32_t Kk = 0u, cutk = kNoCut, n_s = (uint32_t)V;  // S = {key > Kk} U {key == Kk, idx <= cutk}
-  if (mode == MODE_TOPK || mode == MODE_TOPKP) {
+  if (!sorted_out && (mode == MODE_TOPK || mode == MODE_TOPKP)) {
     const uint32_t k = (uint32_t)pl.k;
     const bool hit_ref = sigma && n_c > k;  // is_hit, sigma_trunc.py:127-133
     met.trunc_hit = (hit_ref && !force_fb) ? 1 : 0;
@@ -1160,14 +1320,14 @@ __device__ __forceinline__ void tail_body(const Params &P, uint8_t *dsmem, TailS
     uint32_t ck = k - kr.n_gt;  // n_keep = n_dup - (N - k), pipeline.py:117
     if (nodup) ck = kr.n_eq;
     if (ck >= kr.n_eq) cutk = kNoCut;
-    else cutk = k_used_x ? select_nth_eq(X, Kk, ck, red) : select_nth_eq(RW, Kk, ck, red);
+    else cutk = select_nth_eq(RW, Kk, ck, red);  // index order: scan the row itself
     n_s = kr.n_gt + ck;
     Kf = Kk; cutf = cutk; kept = n_s;
     QRITA_TSTAMP(4);
   }
 
   // ================= top-p stage: pipeline.py:161-196 (p only) and :226-239 (k then p) ============
-  if (mode == MODE_TOPP || mode == MODE_TOPKP) {
+  if (!sorted_out && (mode == MODE_TOPP || mode == MODE_TOPKP)) {
     red.act_key = ak;  // (key, probability) pairs from here on
     const Fx Tp = pl.t_p, Tsp = pl.t_sp;
     const bool topp_only = (mode == MODE_TOPP);
@@ -1283,10 +1443,8 @@ __device__ __forceinline__ void tail_body(const Params &P, uint8_t *dsmem, TailS
       if (j >= pr.n_eq) {
         // whole cluster (within S); if it is the top-k boundary cluster the top-k cut still applies
         cutf = (!topp_only && pr.K == Kk) ? cutk : kNoCut;
-      } else if (set_kind == 2) {
-        cutf = select_nth_eq(RW, pr.K, j, red);
       } else {
-        cutf = select_nth_eq(X, pr.K, j, red);  // X is index-ordered and holds every copy of K
+        cutf = select_nth_eq(RW, pr.K, j, red);  // index order: scan the row itself
       }
     }
   }
@@ -1297,6 +1455,8 @@ __device__ __forceinline__ void tail_body(const Params &P, uint8_t *dsmem, TailS
     write_row<T>(in, out, V, Kf, cutf, inplace ? 2 : 1);  // the stream left top-p-only rows alone
   } else if (inplace) {
     write_row<T>(in, out, V, Kf, cutf, 2);
+  } else if (sorted_out) {
+    for (int q = tid; q < (int)kept; q += kThreads) out[di[q]] = Elem<T>::from_bits(db[q]);
   } else if (k_used_x) {
     for (int i = tid; i < X.n; i += kThreads) {
       const uint32_t b = xb[i];
@@ -1318,9 +1478,7 @@ template <typename T, int NP>
 __global__ void __launch_bounds__(kThreads, 2) qrita_tail(Params P) {
   extern __shared__ __align__(16) uint8_t dsmem[];
   __shared__ TailSmem sm;
-  __shared__ uint32_t s_off[kMaxTailChunks + 1];
-  __shared__ uint32_t s_part[2][kWarps][5];
-  tail_body<T, NP>(P, dsmem, sm, s_off, s_part);
+  tail_body<T, NP>(P, dsmem, sm);
 }
 
 // ------------------------------------------------------------------------------------------------
@@ -1494,21 +1652,35 @@ __global__ void __launch_bounds__(kStreamThreads, 3) qrita_stream(Params P) {
     const uint32_t mx = warp_max(key_of_bits(__float_as_uint(fmx)));
     const uint32_t mn = warp_min(key_of_bits(__float_as_uint(fmn)));
     __syncwarp();
-    const size_t slot = (size_t)item * kCapChunk;
-    const uint32_t nst = base < (uint32_t)kCapChunk ? base : (uint32_t)kCapChunk;
-    // outliers and statistics are re-read by the row tail: keep them in L2 (evict_last) while the
-    // logits stream past with evict_first
-    for (uint32_t j = lane; j < nst; j += 32) {
-      st_keep_u32(P.cand_bits + slot + j, s_cb[wib][j], keep_pol);
-      st_keep_u32(P.cand_idx + slot + j, s_ci[wib][j], keep_pol);
+    // fold the chunk into the row aggregate; reserve room in the row's outlier buffer
+    RowAgg *ag = P.agg + row;
+    uint32_t pos = 0u;
+    if (lane == 0) {
+      if (base) pos = atomicAdd(&ag->count, base);
+      atomicMax(&ag->maxkey, mx);
+      atomicMin(&ag->minkey, mn);
+      if (nf != 0xffffffffu) atomicMin(&ag->nf_col, nf);
+      if (base > (uint32_t)kCapChunk) atomicOr(&ag->ovf, 1u);
     }
-    if (lane == 0) st_keep_u4(reinterpret_cast<uint4 *>(P.cstats + item), make_uint4(mx, base, nf, mn), keep_pol);
+    pos = __shfl_sync(0xffffffffu, pos, 0);
+    const uint32_t nst = base < (uint32_t)kCapChunk ? base : (uint32_t)kCapChunk;
+    const size_t rb = (size_t)row * P.xcap;
+    // outliers are re-read by the row tail: keep them in L2 (evict_last) while the logits stream
+    // past with evict_first
+    for (uint32_t j = lane; j < nst && pos + j < (uint32_t)P.xcap; j += 32) {
+      st_keep_u32(P.cand_bits + rb + pos + j, s_cb[wib][j], keep_pol);
+      st_keep_u32(P.cand_idx + rb + pos + j, s_ci[wib][j], keep_pol);
+    }
     __syncwarp();
+    if (P.exp_publish && lane == 0) {  // EXPERIMENT: per-chunk release of the row counter
+      __threadfence();
+      atomicAdd(&ag->done, 1u);
+    }
   }
   if (!waited) pdl_wait();
 }
 
-constexpr size_t kTailDynSmem = (size_t)kCapX * 8 + (size_t)kCapS * 16 + (size_t)kCapA * 12;
+constexpr size_t kTailDynSmem = (size_t)kCapX * 8 + (size_t)kWorkBytes;
 
 template <typename T, int NP, bool VEC>
 static cudaError_t launch_pipeline(const Params &P, cudaStream_t st, cudaEvent_t prep_done,
@@ -1529,7 +1701,10 @@ static cudaError_t launch_pipeline(const Params &P, cudaStream_t st, cudaEvent_t
     if (want < 1) want = 1;
     stream_grid = sms * (per_sm < want ? (per_sm < 1 ? 1 : per_sm) : want);
   }
-  qrita_prep<T><<<P.B, 256, 0, st>>>(P);
+  Params Pm = P;
+  Pm.exp_publish = getenv("QRITA_EXP_PUBLISH") ? atoi(getenv("QRITA_EXP_PUBLISH")) : 0;
+  const Params &PP = Pm;
+  qrita_prep<T><<<P.B, 256, 0, st>>>(PP);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   if (prep_done) {
@@ -1549,7 +1724,7 @@ static cudaError_t launch_pipeline(const Params &P, cudaStream_t st, cudaEvent_t
   cfg.stream = st;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  e = cudaLaunchKernelEx(&cfg, qrita_stream<T, VEC>, P);
+  e = cudaLaunchKernelEx(&cfg, qrita_stream<T, VEC>, PP);
   if (e != cudaSuccess) return e;
   if (stream_done) {
     e = cudaEventRecord(stream_done, st);
@@ -1559,7 +1734,7 @@ static cudaError_t launch_pipeline(const Params &P, cudaStream_t st, cudaEvent_t
   cfg.gridDim = dim3((unsigned)P.B);
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = kTailDynSmem;
-  return cudaLaunchKernelEx(&cfg, qrita_tail<T, NP>, P);
+  return cudaLaunchKernelEx(&cfg, qrita_tail<T, NP>, PP);
 }
 
 template <typename T>

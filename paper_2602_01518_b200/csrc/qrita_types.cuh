@@ -16,12 +16,26 @@ namespace qrita {
 // ------------------------------------------------------------------------------------------------
 constexpr int kTableSize = 200;  // tables.py:11
 constexpr int kChunk = 1024;     // elements per streaming work item (one warp)
-constexpr int kCapChunk = 256;   // outlier slots per work item in the HBM scratch (25%)
-constexpr int kCapX = 8192;      // outliers staged in shared memory for the row tail
+constexpr int kCapChunk = 256;   // outliers per chunk staged in shared memory by the streaming warp
+constexpr int kCapX = 8192;      // outliers per row: row buffer in HBM and shared-memory staging
+constexpr int kSpecTail = 16;    // outliers per tail thread loaded before the row count is known
 constexpr int kCapS = 1024;      // top-k survivors whose probabilities are cached in shared memory
 constexpr int kCapA = 1024;      // active set of the top-p pivot search (3x as many keys for top-k)
 constexpr int kStreamThreads = 256;
 constexpr int kMaxTailChunks = 2048;  // chunk offsets kept in shared memory by the row tail (V <= 2M)
+// Bin-sort resolve of the row tail (sigma-hit top-k / top-k+top-p rows): the outliers are counted
+// into kNB equal-width key bins while they are staged; the bins from the one holding the k-th key
+// upward (<= kCapC candidates) are counting-sorted, each bin ordered in place (<= kMaxBin entries).
+constexpr int kLogNB = 10;
+constexpr int kNB = 1 << kLogNB;
+constexpr int kCapC = 2048;
+constexpr int kMaxBin = 64;
+// Shared-memory work area behind the staged outliers: the bin-sort layout (counts, cursors, two
+// candidate arrays) or the pivot-search layout (survivors, active sets), whichever is larger.
+constexpr int kWorkBytesSearch = kCapS * 16 + kCapA * 12;
+constexpr int kWorkBytesBins = kNB * 8 + kCapC * 16;
+constexpr int kWorkBytes = kWorkBytesSearch > kWorkBytesBins ? kWorkBytesSearch : kWorkBytesBins;
+static_assert((kMaxTailChunks + 1) * 4 <= kCapC * 8, "chunk offsets alias the candidate array");
 
 enum Mode : int32_t { MODE_INVALID = -1, MODE_PASS = 0, MODE_TOPK = 1, MODE_TOPP = 2, MODE_TOPKP = 3 };
 enum Status : int32_t { ST_BAD_K = 1, ST_BAD_P = 2, ST_NONFINITE = 4 };
@@ -42,11 +56,17 @@ struct alignas(16) RowPlan {
 };
 static_assert(sizeof(RowPlan) % 16 == 0, "RowPlan is copied with 16-byte loads");
 
-struct ChunkStat {
+// Per-row aggregate of the streaming pass, initialised by qrita_prep and updated with atomics by
+// every chunk of the row (qrita_stream): outliers appended so far, row max / min order keys, first
+// non-finite column, overflow flag, chunks finished (the row tail starts when done == nchunks).
+struct alignas(16) RowAgg {
+  uint32_t count;     // outliers of the row (entries beyond the row buffer are dropped)
   uint32_t maxkey;
-  uint32_t count;     // outliers in the chunk (only the first kCapChunk are stored)
-  uint32_t nf_col;    // first non-finite column, or 0xffffffff
   uint32_t minkey;
+  uint32_t nf_col;    // first non-finite column, or 0xffffffff
+  uint32_t ovf;       // some chunk had more outliers than its shared-memory staging holds
+  uint32_t done;      // chunks finished (released after their outliers and output are written)
+  uint32_t pad[2];
 };
 
 // numpy's pairwise-summation tree for the sigma sample (n = min(sample_size, V)), built on the host
@@ -76,39 +96,42 @@ struct Params {
   qrita_row_metrics *metrics;
   // workspace
   RowPlan *plans;
-  ChunkStat *cstats;
-  uint32_t *cand_bits;
-  uint32_t *cand_idx;
+  RowAgg *agg;              // [B]
+  uint32_t *cand_bits;      // [B][xcap] outliers of each row (fp32 bits), in chunk-completion order
+  uint32_t *cand_idx;       // [B][xcap] their column indices
   int32_t *status;
   int32_t *nf_col;
   unsigned long long *dbg;  // [B][16] phase timestamps of the row tail (QRITA_DEBUG_TIMING)
-  uint32_t *row_done;       // [B] chunks of the row finished by qrita_stream (zeroed by qrita_prep)
   int nchunks;
   int total_items;
+  int exp_publish;
+  int xcap;                 // row_cap(V)
   PwTree tree;
 };
 
-// Layout: [status[B] | nf_col[B] | plans[B] | chunk stats | outlier slots].  Every record is fully
-// rewritten by each call (no state carries over), and the status block only depends on B, so
-// qrita_get_status needs no V.
+// Layout: [status[B] | nf_col[B] | dbg | plans[B] | row aggregates[B] | row outlier buffers].  Every
+// record is rewritten by each call (no state carries over), and the status block only depends on
+// B, so qrita_get_status needs no V.
 struct WsLayout {
-  size_t status, nf_col, dbg, row_done, plans, cstats, cand_bits, cand_idx, total;
+  size_t status, nf_col, dbg, plans, agg, cand_bits, cand_idx, total;
 };
 
 inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
+// Outlier buffer entries per row: a row never has more outliers than columns.
+inline __host__ __device__ int row_cap(int V) { return V < kCapX ? V : kCapX; }
+
 inline WsLayout ws_layout(int B, int V) {
   WsLayout L;
-  const size_t nchunks = (size_t)((V + kChunk - 1) / kChunk);
+  const size_t cap = (size_t)row_cap(V);
   size_t off = 0;
   L.status = off;    off = align_up(off + 4ull * (size_t)B, 256);
   L.nf_col = off;    off = align_up(off + 4ull * (size_t)B, 256);
   L.dbg = off;       off = align_up(off + 128ull * (size_t)B, 256);
-  L.row_done = off;  off = align_up(off + 4ull * (size_t)B, 256);
   L.plans = off;     off = align_up(off + sizeof(RowPlan) * (size_t)B, 256);
-  L.cstats = off;    off = align_up(off + sizeof(ChunkStat) * (size_t)B * nchunks, 256);
-  L.cand_bits = off; off = align_up(off + 4ull * (size_t)B * nchunks * kCapChunk, 256);
-  L.cand_idx = off;  off = align_up(off + 4ull * (size_t)B * nchunks * kCapChunk, 256);
+  L.agg = off;       off = align_up(off + sizeof(RowAgg) * (size_t)B, 256);
+  L.cand_bits = off; off = align_up(off + 4ull * (size_t)B * cap, 256);
+  L.cand_idx = off;  off = align_up(off + 4ull * (size_t)B * cap, 256);
   L.total = off;
   return L;
 }

@@ -128,3 +128,12 @@ if len(sys.argv) > 1 and sys.argv[1] == "timing":
             d = np.where(ok, cur - prev, 0)
             print(f"   {nm:8s} mean {d[ok].mean()/1e3 if ok.any() else 0:7.2f} us  max {d.max()/1e3:7.2f}")
             prev = np.where(ok, cur, prev)
+        # bin-sort sub-phases (stamps 10-14 between stageX=2 and ksearch=3)
+        sub = ["binscan", "scatter", "fixup", "expD", "piscan", "cross"]
+        prev = a[:, 2]
+        for j, nm in enumerate(sub):
+            cur = a[:, 10 + j] if j < 5 else a[:, 3]
+            ok = (cur > 0) & (prev > 0)
+            d = np.where(ok, cur - prev, 0)
+            print(f"     {nm:8s} mean {d[ok].mean()/1e3 if ok.any() else 0:7.2f} us  max {d.max()/1e3:7.2f}")
+            prev = np.where(cur > 0, cur, prev)
