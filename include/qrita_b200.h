@@ -53,7 +53,9 @@ enum {
   QRITA_NO_DUP          = 1 << 3, /* duplication_handling_enabled=False: keep whole boundary cluster*/
   QRITA_INPLACE         = 1 << 4, /* out == logits (pipeline.py:72-74)                               */
   QRITA_RESERVED_5      = 1 << 5, /* reserved (rejected)                                            */
-  QRITA_DEBUG_TIMING    = 1 << 6  /* record per-row tail phase timestamps (qrita_get_timing)        */
+  QRITA_DEBUG_TIMING    = 1 << 6, /* record per-row tail phase timestamps (qrita_get_timing)        */
+  QRITA_STAGED          = 1 << 7  /* force the staged 3-kernel pipeline (prep / stream / tail) even
+                                     when the fused single-kernel path applies                      */
 };
 
 /* return codes */

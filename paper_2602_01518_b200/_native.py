@@ -21,6 +21,7 @@ FORCE_FALLBACK = 1 << 2
 NO_DUP = 1 << 3
 INPLACE = 1 << 4
 DEBUG_TIMING = 1 << 6
+STAGED = 1 << 7
 
 OK = 0
 EINVAL_ARG = 1

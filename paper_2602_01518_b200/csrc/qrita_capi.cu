@@ -103,7 +103,7 @@ int qrita_topk_topp_ex(const void *logits, int64_t ld_in, int dtype, int B, int 
   if (B < 1 || V < 1 || ld_in < V || ld_out < V || sample_size < 1) return QRITA_EINVAL_ARG;
   if (dtype != QRITA_DTYPE_F32 && dtype != QRITA_DTYPE_BF16) return QRITA_EINVAL_ARG;
   if (flags & ~(QRITA_SEARCH_BINARY | QRITA_NO_SIGMA | QRITA_FORCE_FALLBACK | QRITA_NO_DUP | QRITA_INPLACE |
-                QRITA_DEBUG_TIMING))
+                QRITA_DEBUG_TIMING | QRITA_STAGED))
     return QRITA_EINVAL_ARG;
   const bool inplace = (flags & QRITA_INPLACE) != 0;
   if (inplace != (logits == out)) return QRITA_EINVAL_ARG;

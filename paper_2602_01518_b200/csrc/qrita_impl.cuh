@@ -167,118 +167,47 @@ __device__ double pairwise_tree(int n, LeafFn leaf) {
   }
 }
 
-template <typename T>
-__global__ void __launch_bounds__(256) qrita_prep(Params P) {
-  __shared__ float s_x[kPwStage];
-  __shared__ double s_acc[2][kPwMaxLeaves][8];
-  __shared__ double s_val[2][2 * kPwMaxLeaves];
-  __shared__ double s_res[2];
+// Row routing (pipeline.py:199-218): which stages run for (k, p).
+__device__ __forceinline__ int row_mode(int64_t k, double p, int V) {
+  const bool bad_k = !(k >= 1 && k <= (int64_t)V);
+  const bool bad_p = !(p > 0.0 && p <= 1.0);
+  if (bad_k || bad_p) return MODE_INVALID;
+  if (k == V && p == 1.0) return MODE_PASS;
+  if (k == V) return MODE_TOPP;
+  if (p == 1.0) return MODE_TOPK;
+  return MODE_TOPKP;
+}
 
-  pdl_launch_dependents();  // the streaming kernel may start loading logits right away
-  const int row = blockIdx.x;
-  const int tid = threadIdx.x;
+// Scratch of the sigma statistics (shared memory, >= 20 KB).
+struct PlanScratch {
+  double acc[2][kPwMaxLeaves][8];
+  double val[2][2 * kPwMaxLeaves];
+  double res[2];
+};
+
+// Per-row plan (sigma_trunc.py:69-103; mode routing of pipeline.py:199-218), in two steps so the
+// sample-independent part overlaps the sample's arrival:
+//   plan_begin (thread 0): mode, table delta (sigma_trunc.py:85-103), exact fixed-point nucleus
+//                          thresholds, status word; writes *out (key_thr / mu / sigma / t pending);
+//   plan_sample (tail thread group, kThreads threads, tsync barriers): numpy's pairwise mean and mean
+//                          square of the sample (bit-replica), sigma, threshold key.  xs(i) returns
+//                          sample element i from shared memory; `a` is the row in global memory
+//                          (serial fallback for long samples).  Reads *out after a barrier.
+__device__ __forceinline__ void plan_begin(const Params &P, int row, RowPlan *out) {
   const int V = P.V;
   const int64_t k = P.k[row];
   const double p = P.p[row];
-  const bool bad_k = !(k >= 1 && k <= (int64_t)V);
-  const bool bad_p = !(p > 0.0 && p <= 1.0);
-  int mode;
-  if (bad_k || bad_p) mode = MODE_INVALID;
-  else if (k == V && p == 1.0) mode = MODE_PASS;
-  else if (k == V) mode = MODE_TOPP;
-  else if (p == 1.0) mode = MODE_TOPK;
-  else mode = MODE_TOPKP;
-
+  const int mode = row_mode(k, p, V);
   const bool want_thr = (mode == MODE_TOPK || mode == MODE_TOPP || mode == MODE_TOPKP) &&
                         !(P.flags & QRITA_NO_SIGMA);
-  double mu = 0.0, sigma = 0.0, t = 0.0;
-  uint32_t key_thr = 0xffffffffu;
-  if (want_thr) {  // uniform per block
-    const T *a = (const T *)P.logits + (size_t)row * P.ld_in;
-    const PwTree &tr = P.tree;
-    const int n = tr.n;
-    const int nl = tr.n_leaves;
-    if (nl > 0) {
-      // batch the loads: 8 independent loads in flight per thread instead of one load per trip
-      constexpr int R = 8;
-      for (int i0 = tid; i0 < n; i0 += 256 * R) {
-        float tmp[R];
-#pragma unroll
-        for (int r = 0; r < R; ++r) {
-          const int i = i0 + r * 256;
-          tmp[r] = i < n ? __uint_as_float(Elem<T>::bits(__ldg(a + i))) : 0.0f;
-        }
-#pragma unroll
-        for (int r = 0; r < R; ++r) {
-          const int i = i0 + r * 256;
-          if (i < n) s_x[i] = tmp[r];
-        }
-      }
-      __syncthreads();
-      // numpy's 8-accumulator leaf loop, one thread per (leaf, accumulator)
-      for (int q = tid; q < nl * 8; q += blockDim.x) {
-        const int L = q >> 3, j = q & 7;
-        const int o = tr.leaf_off[L], m = tr.leaf_len[L];
-        if (m >= 8) {
-          double r0 = (double)s_x[o + j];
-          double r1 = __dmul_rn(r0, r0);
-          for (int i = 8; i < m - (m % 8); i += 8) {
-            const double x = (double)s_x[o + i + j];
-            r0 = __dadd_rn(r0, x);
-            r1 = __dadd_rn(r1, __dmul_rn(x, x));
-          }
-          s_acc[0][L][j] = r0;
-          s_acc[1][L][j] = r1;
-        }
-      }
-      __syncthreads();
-      for (int q = tid; q < nl * 2; q += blockDim.x) {
-        const int L = q >> 1, sq = q & 1;
-        const int o = tr.leaf_off[L], m = tr.leaf_len[L];
-        double res;
-        int i;
-        if (m < 8) {
-          res = 0.0;
-          i = 0;
-        } else {
-          const double *r = s_acc[sq][L];
-          res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
-                          __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
-          i = m - (m % 8);
-        }
-        for (; i < m; ++i) {
-          const double x = (double)s_x[o + i];
-          res = __dadd_rn(res, sq ? __dmul_rn(x, x) : x);
-        }
-        s_val[sq][L] = res;
-      }
-      __syncthreads();
-      // internal nodes level by level: pw(a, n) = pw(a, n2) + pw(a + n2, n - n2)
-      int lo = 0;
-      for (int h = 0; h < tr.n_levels; ++h) {
-        const int hi = tr.level_end[h];
-        for (int q = lo + (tid >> 1); q < hi; q += blockDim.x >> 1) {
-          const int sq = tid & 1;
-          s_val[sq][nl + q] = __dadd_rn(s_val[sq][tr.left[q]], s_val[sq][tr.right[q]]);
-        }
-        lo = hi;
-        __syncthreads();
-      }
-      if (tid < 2) s_res[tid] = s_val[tid][nl + tr.n_internal - 1 < nl ? 0 : nl + tr.n_internal - 1];
-    } else if (tid < 2) {  // long samples (non-default sample_size): serial replay from global
-      s_res[tid] = tid == 0
-          ? pairwise_tree(n, [&](int o, int m) -> double { return leaf_sum<T, false>(a + o, m); })
-          : pairwise_tree(n, [&](int o, int m) -> double { return leaf_sum<T, true>(a + o, m); });
-    }
-    __syncthreads();
-    const double sum = s_res[0], sq = s_res[1];
-    // sigma_trunc.py:78-81 — mean, E[x^2] - mu^2 floored at 0, sqrt; no FMA contraction anywhere.
-    mu = __ddiv_rn(sum, (double)n);
-    const double e2 = __ddiv_rn(sq, (double)n);
-    const double var = __dsub_rn(e2, __dmul_rn(mu, mu));
-    sigma = __dsqrt_rn(var > 0.0 ? var : 0.0);
-    // table lookup (sigma_trunc.py:85-96) and safety margin (sigma_trunc.py:99-103)
-    double delta;
+  RowPlan pl;
+  pl.key_thr = 0xffffffffu;
+  pl.mode = mode;
+  pl.k = k;
+  pl.p = p;
+  pl.mu = pl.sigma = pl.t = 0.0;
+  double delta = 0.0;
+  if (want_thr) {  // table lookup (sigma_trunc.py:85-96); delta parked in t until plan_sample
     if (mode == MODE_TOPP) {
       int idx = (int)__dmul_rn(p, (double)kTableSize);
       delta = c_topp_table[min(idx, kTableSize - 1)];
@@ -286,34 +215,144 @@ __global__ void __launch_bounds__(256) qrita_prep(Params P) {
       int idx = (int)__dmul_rn(__ddiv_rn((double)k, (double)V), (double)kTableSize);
       delta = c_topk_table[min(idx, kTableSize - 1)];
     }
+  }
+  pl.t = delta;
+  if (mode == MODE_TOPP || mode == MODE_TOPKP) {
+    pl.t_p = fx_round_threshold(p);
+    pl.t_sp = fx_round_threshold(nextafter(p, 2.0));
+  } else {
+    pl.t_p = fx_zero();
+    pl.t_sp = fx_zero();
+  }
+  pl.has_thr = want_thr ? 1 : 0;
+  pl.pad[0] = pl.pad[1] = pl.pad[2] = 0;
+  *out = pl;
+  const bool bad_k = !(k >= 1 && k <= (int64_t)V);
+  const bool bad_p = !(p > 0.0 && p <= 1.0);
+  P.status[row] = (bad_k ? ST_BAD_K : 0) | (bad_p ? ST_BAD_P : 0);
+  P.nf_col[row] = -1;
+}
+
+template <typename T, class SampleAt>
+__device__ void plan_sample(const Params &P, SampleAt xs, const T *a, PlanScratch &sc, RowPlan *out) {
+  const int tid = threadIdx.x;
+  if (!out->has_thr) return;  // uniform per group (written before the caller's barrier)
+  const PwTree &tr = P.tree;
+  const int n = tr.n;
+  const int nl = tr.n_leaves;
+  if (nl > 0) {
+    // numpy's 8-accumulator leaf loop, one thread per (leaf, accumulator)
+    for (int q = tid; q < nl * 8; q += kThreads) {
+      const int L = q >> 3, j = q & 7;
+      const int o = tr.leaf_off[L], m = tr.leaf_len[L];
+      if (m >= 8) {
+        double r0 = (double)xs(o + j);
+        double r1 = __dmul_rn(r0, r0);
+        for (int i = 8; i < m - (m % 8); i += 8) {
+          const double x = (double)xs(o + i + j);
+          r0 = __dadd_rn(r0, x);
+          r1 = __dadd_rn(r1, __dmul_rn(x, x));
+        }
+        sc.acc[0][L][j] = r0;
+        sc.acc[1][L][j] = r1;
+      }
+    }
+    tsync();
+    for (int q = tid; q < nl * 2; q += kThreads) {
+      const int L = q >> 1, sq = q & 1;
+      const int o = tr.leaf_off[L], m = tr.leaf_len[L];
+      double res;
+      int i;
+      if (m < 8) {
+        res = 0.0;
+        i = 0;
+      } else {
+        const double *r = sc.acc[sq][L];
+        res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                        __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+        i = m - (m % 8);
+      }
+      for (; i < m; ++i) {
+        const double x = (double)xs(o + i);
+        res = __dadd_rn(res, sq ? __dmul_rn(x, x) : x);
+      }
+      sc.val[sq][L] = res;
+    }
+    tsync();
+    // internal nodes level by level: pw(a, n) = pw(a, n2) + pw(a + n2, n - n2)
+    int lo = 0;
+    for (int h = 0; h < tr.n_levels; ++h) {
+      const int hi = tr.level_end[h];
+      for (int q = lo + (tid >> 1); q < hi; q += kThreads >> 1) {
+        const int sq = tid & 1;
+        sc.val[sq][nl + q] = __dadd_rn(sc.val[sq][tr.left[q]], sc.val[sq][tr.right[q]]);
+      }
+      lo = hi;
+      tsync();
+    }
+    if (tid < 2) sc.res[tid] = sc.val[tid][nl + tr.n_internal - 1 < nl ? 0 : nl + tr.n_internal - 1];
+  } else if (tid < 2) {  // long samples (non-default sample_size): serial replay from global
+    sc.res[tid] = tid == 0
+        ? pairwise_tree(n, [&](int o, int m) -> double { return leaf_sum<T, false>(a + o, m); })
+        : pairwise_tree(n, [&](int o, int m) -> double { return leaf_sum<T, true>(a + o, m); });
+  }
+  tsync();
+  if (tid == 0) {
+    const double sum = sc.res[0], sq = sc.res[1];
+    // sigma_trunc.py:78-81 — mean, E[x^2] - mu^2 floored at 0, sqrt; no FMA contraction anywhere.
+    const double mu = __ddiv_rn(sum, (double)n);
+    const double e2 = __ddiv_rn(sq, (double)n);
+    const double var = __dsub_rn(e2, __dmul_rn(mu, mu));
+    const double sigma = __dsqrt_rn(var > 0.0 ? var : 0.0);
+    // safety margin (sigma_trunc.py:99-103)
+    const double delta = out->t;
     const double delta_adj = __dsub_rn(delta, __dmul_rn(0.2, fabs(delta)));
-    t = __dadd_rn(mu, __dmul_rn(delta_adj, sigma));
+    const double t = __dadd_rn(mu, __dmul_rn(delta_adj, sigma));
     // outlier iff float64(z) > t  <=>  z >= f where f is the smallest float above t
     float f = __double2float_rd(t);
     if (!((double)f > t)) f = nextafterf(f, __uint_as_float(0x7f800000u));
-    key_thr = key_of_bits(__float_as_uint(f));
+    out->key_thr = key_of_bits(__float_as_uint(f));
+    out->mu = mu;
+    out->sigma = sigma;
+    out->t = t;
   }
-  if (tid == 0) {
-    RowPlan pl;
-    pl.key_thr = key_thr;
-    pl.mode = mode;
-    pl.k = k;
-    pl.p = p;
-    pl.mu = mu;
-    pl.sigma = sigma;
-    pl.t = t;
-    if (mode == MODE_TOPP || mode == MODE_TOPKP) {
-      pl.t_p = fx_round_threshold(p);
-      pl.t_sp = fx_round_threshold(nextafter(p, 2.0));
-    } else {
-      pl.t_p = fx_zero();
-      pl.t_sp = fx_zero();
+}
+
+// K0 of the staged pipeline: one CTA per row stages the sample prefix and writes the row's plan and
+// initialises its streaming aggregate.
+template <typename T>
+__global__ void __launch_bounds__(kThreads) qrita_prep(Params P) {
+  __shared__ float s_x[kPwStage];
+  __shared__ PlanScratch sc;
+  __shared__ RowPlan s_pl;
+  pdl_launch_dependents();  // the streaming kernel may start loading logits right away
+  const int row = blockIdx.x;
+  const int tid = threadIdx.x;
+  const T *a = (const T *)P.logits + (size_t)row * P.ld_in;
+  const int n = P.tree.n;
+  if (P.tree.n_leaves > 0) {
+    // batch the loads: 8 independent loads in flight per thread instead of one load per trip
+    constexpr int R = 8;
+    for (int i0 = tid; i0 < n; i0 += kThreads * R) {
+      float tmp[R];
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const int i = i0 + r * kThreads;
+        tmp[r] = i < n ? __uint_as_float(Elem<T>::bits(__ldg(a + i))) : 0.0f;
+      }
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const int i = i0 + r * kThreads;
+        if (i < n) s_x[i] = tmp[r];
+      }
     }
-    pl.has_thr = want_thr ? 1 : 0;
-    pl.pad[0] = pl.pad[1] = pl.pad[2] = 0;
-    P.plans[row] = pl;
-    P.status[row] = (bad_k ? ST_BAD_K : 0) | (bad_p ? ST_BAD_P : 0);
-    P.nf_col[row] = -1;
+  }
+  if (tid == 0) plan_begin(P, row, &s_pl);
+  tsync();
+  plan_sample<T>(P, [&](int i) -> float { return s_x[i]; }, a, sc, &s_pl);
+  tsync();
+  if (tid == 0) {
+    P.plans[row] = s_pl;
     uint4 *ag = reinterpret_cast<uint4 *>(P.agg + row);
     ag[0] = make_uint4(0u, 0u, 0xffffffffu, 0xffffffffu);  // count, maxkey, minkey, nf_col
     ag[1] = make_uint4(0u, 0u, 0u, 0u);                     // ovf, done
@@ -356,7 +395,7 @@ __device__ __forceinline__ uint32_t block_exscan_u32(uint32_t v, uint32_t *buf, 
     if (lane >= o) incl += u;
   }
   if (lane == 31) buf[warp] = incl;
-  __syncthreads();
+  tsync();
   uint32_t before = 0u, tot = 0u;
 #pragma unroll
   for (int w = 0; w < kWarps; ++w) {
@@ -380,7 +419,7 @@ __device__ __forceinline__ Fx block_exscan_fx(const Fx &v, Fx *buf, Fx &total) {
     if (lane >= o) incl = fx_add(incl, u);
   }
   if (lane == 31) buf[warp] = incl;
-  __syncthreads();
+  tsync();
   Fx before = fx_zero(), tot = fx_zero();
 #pragma unroll
   for (int w = 0; w < kWarps; ++w) {
@@ -441,6 +480,46 @@ struct SrcRow {  // the full row in global memory
   }
 };
 
+// Batched element visits: kLd loads in flight per thread before any is used, so passes over the
+// row in global memory are bandwidth- rather than latency-bound.  for_elems calls fn(i, bits, idx)
+// for i = tid, tid + kThreads, ... < n.  for_elems_warp keeps whole warps converged (for warp-
+// aggregated slot reservation): fn(i, valid, bits, idx) is called by every lane.
+constexpr int kLd = 4;
+template <class Src, class Fn>
+__device__ __forceinline__ void for_elems(const Src &src, int n, Fn fn) {
+  for (int i0 = threadIdx.x; i0 < n; i0 += kThreads * kLd) {
+    uint32_t b[kLd], x[kLd];
+#pragma unroll
+    for (int j = 0; j < kLd; ++j) {
+      const int i = i0 + j * kThreads;
+      b[j] = x[j] = 0u;
+      if (i < n) src.get(i, b[j], x[j]);
+    }
+#pragma unroll
+    for (int j = 0; j < kLd; ++j) {
+      const int i = i0 + j * kThreads;
+      if (i < n) fn(i, b[j], x[j]);
+    }
+  }
+}
+template <class Src, class Fn>
+__device__ __forceinline__ void for_elems_warp(const Src &src, int n, Fn fn) {
+  for (int i0 = threadIdx.x; i0 - (int)threadIdx.x < n; i0 += kThreads * kLd) {
+    uint32_t b[kLd], x[kLd];
+#pragma unroll
+    for (int j = 0; j < kLd; ++j) {
+      const int i = i0 + j * kThreads;
+      b[j] = x[j] = 0u;
+      if (i < n) src.get(i, b[j], x[j]);
+    }
+#pragma unroll
+    for (int j = 0; j < kLd; ++j) {
+      const int i = i0 + j * kThreads;
+      fn(i, i < n, b[j], x[j]);
+    }
+  }
+}
+
 // Pivot-pass statistics.  Bucket j holds keys in (piv[j], piv[j+1]], piv[NP] = +inf; keys <= piv[0]
 // are ignored.  Per bucket: count, min key, count of the min key, exact mass.
 template <int NP, bool MASS>
@@ -499,7 +578,7 @@ __device__ void bk_reduce(Buckets<NP, MASS> &b, Red &R) {
       }
     }
   }
-  __syncthreads();
+  tsync();
   const bool act = lane < kWarps;
 #pragma unroll
   for (int j = 0; j < NP; ++j) {
@@ -585,12 +664,10 @@ template <class Src, class Fn>
 __device__ Fx block_mass(const Src &src, Fn fn, uint32_t &count, Red &R) {
   Buckets<1, true> b;
   b.cnt[0] = 0u; b.mn[0] = 0u; b.mc[0] = 0u; b.ms[0] = fx_zero();
-  for (int i = threadIdx.x; i < src.n; i += kThreads) {
-    uint32_t bits, ix;
-    src.get(i, bits, ix);
+  for_elems(src, src.n, [&](int i, uint32_t bits, uint32_t ix) {
     double v;
     if (fn(bits, ix, i, v)) { b.ms[0] = fx_add(b.ms[0], fx_from_double(v)); b.cnt[0] += 1u; }
-  }
+  });
   bk_reduce(b, R);
   count = b.cnt[0];
   return b.ms[0];
@@ -607,8 +684,8 @@ __device__ __forceinline__ int bracket_shift(uint32_t w) {  // smallest s with w
   return lg - 8;
 }
 
-template <bool MASS, class KeyOf, class PiOf>
-__device__ void bracket_pass(int n, KeyOf key_of, PiOf pi_of, uint32_t k, const Fx &T, Red &R,
+template <bool MASS, class Src, class Acc, class PiOf>
+__device__ void bracket_pass(const Src &src, Acc acc, PiOf pi_of, uint32_t k, const Fx &T, Red &R,
                              const Fx *T_keep_all = nullptr) {
   SearchState &st = R.sm.st;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -619,23 +696,22 @@ __device__ void bracket_pass(int n, KeyOf key_of, PiOf pi_of, uint32_t k, const 
 #pragma unroll
     for (int q = 0; q < 5; ++q) R.hms[q * kBins + tid] = 0ull;
   }
-  __syncthreads();
-  for (int i = tid; i < n; i += kThreads) {
-    uint32_t key;
-    if (!key_of(i, key)) continue;
-    if (key <= l || key > r) continue;
+  tsync();
+  for_elems(src, src.n, [&](int i, uint32_t bits, uint32_t ix) {
+    const uint32_t key = key_of_bits(bits);
+    if (key <= l || key > r || !acc(key, ix)) return;
     const uint32_t b = (key - l - 1u) >> sh;
     atomicAdd(&R.hcnt[b], 1u);
     if (MASS) {
-      const Fx f = fx_from_double(pi_of(i));
+      const Fx f = fx_from_double(pi_of(bits, i));
       const uint32_t pc[5] = {(uint32_t)f.w0, (uint32_t)(f.w0 >> 32), (uint32_t)f.w1,
                               (uint32_t)(f.w1 >> 32), (uint32_t)f.w2};
 #pragma unroll
       for (int q = 0; q < 5; ++q)
         if (pc[q]) atomicAdd(&R.hms[q * kBins + b], (unsigned long long)pc[q]);
     }
-  }
-  __syncthreads();
+  });
+  tsync();
   // suffix scan over buckets: thread t holds bucket b = 255 - t, so a prefix over t is a suffix over b
   const int b = kBins - 1 - tid;
   const uint32_t c = R.hcnt[b];
@@ -672,7 +748,7 @@ __device__ void bracket_pass(int n, KeyOf key_of, PiOf pi_of, uint32_t k, const 
     R.sm.ctot[warp] = ci;
     if (MASS) R.sm.mtot[warp] = mi;
   }
-  __syncthreads();
+  tsync();
   uint32_t above = cr;  // keys above this warp's buckets (higher buckets live in lower warps)
   Fx mab = st.Mr;
   for (int w = 0; w < warp; ++w) {
@@ -688,7 +764,7 @@ __device__ void bracket_pass(int n, KeyOf key_of, PiOf pi_of, uint32_t k, const 
     st.cl = suf;
     st.compact = fx_ge(msuf, *T_keep_all) ? 0 : 2;  // 2 = keep all
   }
-  __syncthreads();
+  tsync();
   if (MASS && T_keep_all && st.compact == 2) return;
   // the crossing bucket: reaches the target with itself, misses it without
   const bool in = MASS ? fx_ge(msuf, T) : (suf >= k);
@@ -707,7 +783,7 @@ __device__ void bracket_pass(int n, KeyOf key_of, PiOf pi_of, uint32_t k, const 
     }
     st.iters += 1;
   }
-  __syncthreads();
+  tsync();
 }
 
 template <int NP, class Src>
@@ -717,19 +793,16 @@ __device__ KRes search_k(const Src &src, uint32_t l, uint32_t r, uint32_t cl, ui
   if (threadIdx.x == 0) {
     st.l = l; st.r = r; st.cl = cl; st.cr = cr; st.done = 0u; st.iters = 0; st.compact = 0; st.n_act = 0u;
   }
-  __syncthreads();
+  tsync();
   const Fx zero = fx_zero();
   if (r - l > (uint32_t)(4 * kBins)) {
-    bracket_pass<false>(src.n, [&](int i, uint32_t &key) {
-      uint32_t bits, ix;
-      src.get(i, bits, ix);
-      key = key_of_bits(bits);
-      return true; }, [&](int) { return 0.0; }, k, zero, R);
+    bracket_pass<false>(src, [&](uint32_t, uint32_t) { return true; },
+                        [&](uint32_t, int) { return 0.0; }, k, zero, R);
     if (threadIdx.x == 0 && !st.done) {
       const uint32_t n_in = st.cl - st.cr;
       if ((int)n_in <= R.act_cap_k && 2 * (int)n_in <= src.n) st.compact = 1;
     }
-    __syncthreads();
+    tsync();
   }
   bool act = false;  // searching the compacted active set instead of src
   for (;;) {
@@ -737,42 +810,36 @@ __device__ KRes search_k(const Src &src, uint32_t l, uint32_t r, uint32_t cl, ui
     if (st.done || r - l <= 1u) break;
     if (st.compact && !act) {
       // keep only the keys that can still matter: (l, r]  (order is irrelevant to counts)
-      for (int i0 = 0; i0 < src.n; i0 += kThreads) {
-        const int i = i0 + threadIdx.x;
-        uint32_t key = 0u;
-        if (i < src.n) {
-          uint32_t bits, ix;
-          src.get(i, bits, ix);
-          key = key_of_bits(bits);
-        }
-        const bool keep = i < src.n && key > l && key <= r;
+      for_elems_warp(src, src.n, [&](int, bool valid, uint32_t bits, uint32_t) {
+        const uint32_t key = key_of_bits(bits);
+        const bool keep = valid && key > l && key <= r;
         const uint32_t pos = warp_reserve(&st.n_act, keep);
         if (keep) R.act_key[pos] = key;
-      }
+      });
       act = true;
-      __syncthreads();
+      tsync();
     }
     const int n = act ? (int)st.n_act : src.n;
     uint32_t piv[NP];
     make_pivots<NP>(l, r, piv);
     Buckets<NP, false> b;
     bk_init(b);
-    for (int i = threadIdx.x; i < n; i += kThreads) {
-      uint32_t key;
-      if (act) {
-        key = R.act_key[i];
-      } else {
-        uint32_t bits, ix;
-        src.get(i, bits, ix);
-        key = key_of_bits(bits);
+    // only keys inside (piv[0], r] can move a decision; everything above r is the known cr
+    if (act) {
+      for (int i = threadIdx.x; i < n; i += kThreads) {
+        const uint32_t key = R.act_key[i];
+        if (key > piv[0] && key <= r) bk_add(b, piv, key, zero);
       }
-      // only keys inside (piv[0], r] can move a decision; everything above r is the known cr
-      if (key > piv[0] && key <= r) bk_add(b, piv, key, zero);
+    } else {
+      for_elems(src, n, [&](int, uint32_t bits, uint32_t) {
+        const uint32_t key = key_of_bits(bits);
+        if (key > piv[0] && key <= r) bk_add(b, piv, key, zero);
+      });
     }
     uint32_t(*red)[48] = R.sm.red[R.par];
     R.par ^= 1;
     bk_warp_partials(b, red);
-    __syncthreads();
+    tsync();
     if (threadIdx.x < 32) {
       bk_warp0_totals(b, red);
       uint32_t cnt[NP], mn[NP], mc[NP];
@@ -798,11 +865,11 @@ __device__ KRes search_k(const Src &src, uint32_t l, uint32_t r, uint32_t cl, ui
         }
       }
     }
-    __syncthreads();
+    tsync();
   }
   const KRes res = st.done ? KRes{st.K, st.n_gt, st.n_eq, st.iters}
                            : KRes{st.r, st.cr, st.cl - st.cr, st.iters};
-  __syncthreads();
+  tsync();
   return res;
 }
 
@@ -831,28 +898,21 @@ __device__ PRes search_p(const Src &src, uint32_t l, uint32_t r, const Fx &T, co
     st.l = l; st.r = r; st.cl = 0u; st.cr = 0u; st.Ml = Ml; st.Mr = Mr; st.done = 0u; st.iters = 0;
     st.compact = 0; st.n_act = 0u;
   }
-  __syncthreads();
+  tsync();
   if (r - l > (uint32_t)(4 * kBins)) {
-    bracket_pass<true>(src.n, [&](int i, uint32_t &key) {
-      uint32_t bits, ix;
-      src.get(i, bits, ix);
-      key = key_of_bits(bits);
-      return in_s(key, ix); }, [&](int i) {
-      uint32_t bits, ix;
-      src.get(i, bits, ix);
-      return pi_of(bits, i); }, 0u, T, R, &Tsp);
+    bracket_pass<true>(src, in_s, pi_of, 0u, T, R, &Tsp);
     if (st.compact == 2) {  // keep everything
       PRes res{};
       res.keep_all = true;
       res.total = st.Ml;
-      __syncthreads();
+      tsync();
       return res;
     }
     if (threadIdx.x == 0 && !st.done) {
       const uint32_t n_in = st.cl - st.cr;
       if ((int)n_in <= R.act_cap_p && 2 * (int)n_in <= src.n) st.compact = 1;
     }
-    __syncthreads();
+    tsync();
   } else {
     uint32_t cnt;
     const Fx tot = block_mass(src, [&](uint32_t bits, uint32_t ix, int i, double &v) {
@@ -865,7 +925,7 @@ __device__ PRes search_p(const Src &src, uint32_t l, uint32_t r, const Fx &T, co
       return res;
     }
     if (threadIdx.x == 0) { st.cl = cnt; st.Ml = tot; }
-    __syncthreads();
+    tsync();
   }
   bool act = false;
   for (;;) {
@@ -874,40 +934,35 @@ __device__ PRes search_p(const Src &src, uint32_t l, uint32_t r, const Fx &T, co
     Mr = st.Mr;
     if (st.compact && !act) {
       // survivors in (l, r] with their probabilities: later passes need neither src nor exp()
-      for (int i0 = 0; i0 < src.n; i0 += kThreads) {
-        const int i = i0 + threadIdx.x;
-        uint32_t key = 0u, bits = 0u, ix = 0u;
-        if (i < src.n) {
-          src.get(i, bits, ix);
-          key = key_of_bits(bits);
-        }
-        const bool keep = i < src.n && key > l && key <= r && in_s(key, ix);
+      for_elems_warp(src, src.n, [&](int i, bool valid, uint32_t bits, uint32_t ix) {
+        const uint32_t key = key_of_bits(bits);
+        const bool keep = valid && key > l && key <= r && in_s(key, ix);
         const uint32_t pos = warp_reserve(&st.n_act, keep);
         if (keep) { R.act_key[pos] = key; R.act_pi[pos] = pi_of(bits, i); }
-      }
+      });
       act = true;
-      __syncthreads();
+      tsync();
     }
     const int n = act ? (int)st.n_act : src.n;
     uint32_t piv[NP];
     make_pivots<NP>(l, r, piv);
     Buckets<NP, true> b;
     bk_init(b);
-    for (int i = threadIdx.x; i < n; i += kThreads) {
-      if (act) {
+    if (act) {
+      for (int i = threadIdx.x; i < n; i += kThreads) {
         const uint32_t key = R.act_key[i];
         if (key > piv[0] && key <= r) bk_add(b, piv, key, fx_from_double(R.act_pi[i]));
-      } else {
-        uint32_t bits, ix;
-        src.get(i, bits, ix);
+      }
+    } else {
+      for_elems(src, n, [&](int i, uint32_t bits, uint32_t ix) {
         const uint32_t key = key_of_bits(bits);
         if (key > piv[0] && key <= r && in_s(key, ix)) bk_add(b, piv, key, fx_from_double(pi_of(bits, i)));
-      }
+      });
     }
     uint32_t(*red)[48] = R.sm.red[R.par];
     R.par ^= 1;
     bk_warp_partials(b, red);
-    __syncthreads();
+    tsync();
     if (threadIdx.x < 32) {
       bk_warp0_totals(b, red);
       uint32_t cnt[NP], mn[NP], mc[NP];
@@ -950,11 +1005,11 @@ __device__ PRes search_p(const Src &src, uint32_t l, uint32_t r, const Fx &T, co
         }
       }
     }
-    __syncthreads();
+    tsync();
   }
   const PRes res = st.done ? PRes{st.K, st.n_gt, st.n_eq, st.H, st.iters, false, fx_zero()}
                            : PRes{st.r, st.cr, st.cl - st.cr, st.Mr, st.iters, false, fx_zero()};
-  __syncthreads();
+  tsync();
   return res;
 }
 
@@ -975,18 +1030,23 @@ __device__ uint32_t select_nth_eq(const Src &src, uint32_t K, uint32_t c, Red &R
   const int seg = ((n + kWarps - 1) / kWarps + 31) & ~31;
   const int beg = warp * seg, end = min(n, beg + seg);
   uint32_t cnt = 0u;
-  for (int base = beg; base < end; base += 32) {
-    const int i = base + lane;
-    bool m = false;
-    if (i < end) {
-      uint32_t bits, ix;
-      src.get(i, bits, ix);
-      m = key_of_bits(bits) == K;
+  for (int base = beg; base < end; base += 32 * kLd) {  // kLd rows of 32 loads in flight per warp
+    uint32_t b[kLd];
+#pragma unroll
+    for (int j = 0; j < kLd; ++j) {
+      const int i = base + 32 * j + lane;
+      uint32_t ix;
+      b[j] = 0u;
+      if (i < end) src.get(i, b[j], ix);
     }
-    cnt += __popc(__ballot_sync(0xffffffffu, m));
+#pragma unroll
+    for (int j = 0; j < kLd; ++j) {
+      const int i = base + 32 * j + lane;
+      cnt += __popc(__ballot_sync(0xffffffffu, i < end && key_of_bits(b[j]) == K));
+    }
   }
   if (lane == 0) sm.sel[warp] = cnt;
-  __syncthreads();
+  tsync();
   if (threadIdx.x == 0) {
     uint32_t acc = 0u;
     int w = 0;
@@ -998,31 +1058,38 @@ __device__ uint32_t select_nth_eq(const Src &src, uint32_t K, uint32_t c, Red &R
     sm.u[1] = c - acc;
     sm.u[2] = kNoCut;
   }
-  __syncthreads();
+  tsync();
   const int w_star = (int)sm.u[0];
   if (warp == w_star) {
     uint32_t need = sm.u[1];
-    for (int base = beg; base < end; base += 32) {
-      const int i = base + lane;
-      bool m = false;
-      uint32_t ix = 0u;
-      if (i < end) {
-        uint32_t bits;
-        src.get(i, bits, ix);
-        m = key_of_bits(bits) == K;
+    bool found = false;
+    for (int base = beg; base < end && !found; base += 32 * kLd) {
+      uint32_t b[kLd], x[kLd];
+#pragma unroll
+      for (int j = 0; j < kLd; ++j) {
+        const int i = base + 32 * j + lane;
+        b[j] = x[j] = 0u;
+        if (i < end) src.get(i, b[j], x[j]);
       }
-      const uint32_t bal = __ballot_sync(0xffffffffu, m);
-      const uint32_t pc = (uint32_t)__popc(bal);
-      if (pc >= need) {
-        if (lane == nth_set_bit(bal, need)) sm.u[2] = ix;
-        break;
+#pragma unroll
+      for (int j = 0; j < kLd; ++j) {
+        const int i = base + 32 * j + lane;
+        const uint32_t bal = __ballot_sync(0xffffffffu, i < end && key_of_bits(b[j]) == K);
+        const uint32_t pc = (uint32_t)__popc(bal);
+        if (!found) {
+          if (pc >= need) {
+            if (lane == nth_set_bit(bal, need)) sm.u[2] = x[j];
+            found = true;
+          } else {
+            need -= pc;
+          }
+        }
       }
-      need -= pc;
     }
   }
-  __syncthreads();
+  tsync();
   const uint32_t res = sm.u[2];
-  __syncthreads();
+  tsync();
   return res;
 }
 
@@ -1034,78 +1101,67 @@ __device__ __forceinline__ bool kept_by(uint32_t key, uint32_t idx, uint32_t K, 
 // 2 = -inf where not kept (in-place).
 template <typename T>
 __device__ void write_row(const T *in, T *out, int V, uint32_t K, uint32_t cut, int how) {
-  for (int i = threadIdx.x; i < V; i += kThreads) {
-    const T v = in[i];
-    const bool kp = kept_by(key_of_bits(Elem<T>::bits(v)), (uint32_t)i, K, cut);
-    if (how == 0) { if (kp) out[i] = v; }
-    else if (how == 1) { out[i] = kp ? v : Elem<T>::neg_inf(); }
-    else { if (!kp) out[i] = Elem<T>::neg_inf(); }
+  for (int i0 = threadIdx.x; i0 < V; i0 += kThreads * kLd) {
+    T v[kLd];
+#pragma unroll
+    for (int j = 0; j < kLd; ++j) {
+      const int i = i0 + j * kThreads;
+      if (i < V) v[j] = in[i];
+    }
+#pragma unroll
+    for (int j = 0; j < kLd; ++j) {
+      const int i = i0 + j * kThreads;
+      if (i >= V) continue;
+      const bool kp = kept_by(key_of_bits(Elem<T>::bits(v[j])), (uint32_t)i, K, cut);
+      if (how == 0) { if (kp) out[i] = v[j]; }
+      else if (how == 1) { out[i] = kp ? v[j] : Elem<T>::neg_inf(); }
+      else { if (!kp) out[i] = Elem<T>::neg_inf(); }
+    }
   }
 }
 
+// Debug phase timestamps of the row tail (QRITA_DEBUG_TIMING): P.dbg[row][i] = %globaltimer.
+__device__ __forceinline__ void tail_stamp(const Params &P, int row, int i) {
+  if ((P.flags & QRITA_DEBUG_TIMING) && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    P.dbg[(size_t)row * 16 + i] = t;
+  }
+}
+#define QRITA_TSTAMP(i) tail_stamp(P, row, (i))
+
+// Row tail proper, run by the tail thread group (kThreads threads, tsync barriers) once the row's
+// outliers X = (xb, xi)[0, n_c) are in shared memory (in any order; only when they fit: n_c <= kCapX
+// and !overflow) and its aggregates are known: search + duplicate trimming + output of
+// pipeline.py:88-239 with the oracle's semantics (oracle.py:70-89).  `work` is kWorkBytes of shared
+// memory.  Writes the kept logits (the -inf / copy background was written by the streaming pass,
+// except for top-p-only and in-place rows, which are written here in full), kept_count, metrics and
+// the non-finite status.
 template <typename T, int NP>
-__device__ __forceinline__ void tail_body(const Params &P, uint8_t *dsmem, TailSmem &sm) {
-  const int row = blockIdx.x;
-  pdl_wait();  // outliers and chunk statistics of qrita_stream (and plans of qrita_prep)
-  const bool dbg = (P.flags & QRITA_DEBUG_TIMING) != 0;
-#define QRITA_TSTAMP(i)                                                                 \
-  do {                                                                                  \
-    if (dbg && threadIdx.x == 0) {                                                      \
-      unsigned long long t_;                                                            \
-      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                            \
-      P.dbg[(size_t)blockIdx.x * 16 + (i)] = t_;                                        \
-    }                                                                                   \
-  } while (0)
-  QRITA_TSTAMP(0);
+__device__ void tail_resolve(const Params &P, int row, const RowPlan &pl, uint32_t *xb, uint32_t *xi,
+                             uint8_t *work, TailSmem &sm, uint32_t n_c, bool overflow, uint32_t maxkey,
+                             uint32_t minkey, uint32_t nf_col, uint32_t xcap) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int V = P.V;
-  RowPlan pl;
-  {
-    const uint4 *src4 = reinterpret_cast<const uint4 *>(P.plans + row);
-    uint4 *dst4 = reinterpret_cast<uint4 *>(&pl);
-#pragma unroll
-    for (int i = 0; i < (int)(sizeof(RowPlan) / 16); ++i) dst4[i] = __ldcg(src4 + i);
-  }
   const T *in = (const T *)P.logits + (size_t)row * P.ld_in;
   T *out = (T *)P.out + (size_t)row * P.ld_out;
   const bool inplace = (P.flags & QRITA_INPLACE) != 0;
   const bool nodup = (P.flags & QRITA_NO_DUP) != 0;
   const bool force_fb = (P.flags & QRITA_FORCE_FALLBACK) != 0;
-
-  uint32_t *xb = (uint32_t *)dsmem;      // [kCapX] outlier bits
-  uint32_t *xi = xb + kCapX;             // [kCapX] outlier indices
-  uint32_t *sb = xi + kCapX;             // [kCapS] survivor bits
+  uint32_t *sb = (uint32_t *)work;       // [kCapS] survivor bits
   uint32_t *si = sb + kCapS;             // [kCapS] survivor indices
   double *sp = (double *)(si + kCapS);   // [kCapS] survivor exp / probability
   double *ap = sp + kCapS;               // [kCapA] active-set probabilities (top-p search)
   uint32_t *ak = (uint32_t *)(ap + kCapA);  // [kCapA] active-set keys (3*kCapA keys for top-k)
   // bin-sort layout of the same work area
-  uint32_t *hc = sb;                     // [kNB] outliers per key bin
+  uint32_t *hc = (uint32_t *)work;       // [kNB] outliers per key bin
   uint32_t *he = hc + kNB;               // [kNB] bin starts (descending order) -> cursors -> ends
   uint32_t *cb = he + kNB;               // [kCapC] candidates grouped by bin: bits
   uint32_t *ci = cb + kCapC;             //                                     indices
   uint32_t *db = ci + kCapC;             // [kCapC] candidates sorted (key desc, index asc): bits
   uint32_t *di = db + kCapC;             //                                                  indices
   double *ev = (double *)cb;             // [kCapC] survivor exp values (after the sort)
-  for (int i = tid; i < kNB; i += kThreads) hc[i] = 0u;
-
-  // ---- one round trip: the row aggregate, and speculatively the first kSpecTail * kThreads
-  // outliers of the row buffer (coalesced; entries past the count are ignored)
-  const size_t rb = (size_t)row * P.xcap;
-  const uint4 a0 = __ldcg(reinterpret_cast<const uint4 *>(P.agg + row));
-  const uint4 a1 = __ldcg(reinterpret_cast<const uint4 *>(P.agg + row) + 1);
-  uint32_t vb[kSpecTail], vi[kSpecTail];
-#pragma unroll
-  for (int j = 0; j < kSpecTail; ++j) {
-    const int i = tid + j * kThreads;
-    vb[j] = vi[j] = 0u;
-    if (i < P.xcap) { vb[j] = __ldcg(P.cand_bits + rb + i); vi[j] = __ldcg(P.cand_idx + rb + i); }
-  }
-  const uint32_t n_c = a0.x, maxkey = a0.y, minkey = a0.z, nf_col = a0.w;
-  const bool overflow = a1.x != 0u || n_c > (uint32_t)P.xcap;
   const uint32_t lo_row = minkey ? minkey - 1u : 0u;  // below every key of the row
-  __syncthreads();  // bin counters zeroed
-  QRITA_TSTAMP(1);
 
   qrita_row_metrics met;
   memset(&met, 0, sizeof(met));
@@ -1115,7 +1171,7 @@ __device__ __forceinline__ void tail_body(const Params &P, uint8_t *dsmem, TailS
       if (bits_nonfinite(Elem<T>::bits(in[i]))) { first = (uint32_t)i; break; }
     first = warp_min(first);
     if (lane == 0) sm.sel[warp] = first;
-    __syncthreads();
+    tsync();
     if (tid == 0) {
       for (int w = 0; w < kWarps; ++w) first = min(first, sm.sel[w]);
       P.status[row] |= ST_NONFINITE;
@@ -1137,42 +1193,27 @@ __device__ __forceinline__ void tail_body(const Params &P, uint8_t *dsmem, TailS
   const bool sigma = pl.has_thr != 0;
   const double m = value_of_key(maxkey);
   met.outlier_count = sigma ? (int32_t)n_c : 0;
-
-  // ---- stage the outliers in shared memory when they fit
-  const bool x_fits = sigma && !overflow && n_c <= (uint32_t)kCapX;
+  const bool x_fits = sigma && !overflow && n_c <= xcap;
   // bin-sort resolve: sigma hit (count > k, sigma_trunc.py:127-133) of a top-k / top-k+top-p row
   const bool bins = x_fits && NP == 3 && !force_fb && !nodup && (mode == MODE_TOPK || mode == MODE_TOPKP) &&
                     pl.k <= (int64_t)kCapC && n_c > (uint32_t)pl.k;
   const uint32_t bl = pl.key_thr ? pl.key_thr - 1u : 0u;  // every outlier key is > bl
   const int bsh = bin_shift(maxkey - bl);
-  if (x_fits) {
-    // outliers in chunk-completion order (each chunk's run is in index order); bins counted on the way
-#pragma unroll
-    for (int j = 0; j < kSpecTail; ++j) {
-      const uint32_t i = (uint32_t)(tid + j * kThreads);
-      if (i < n_c) {
-        xb[i] = vb[j]; xi[i] = vi[j];
-        if (bins) atomicAdd(&hc[(key_of_bits(vb[j]) - bl - 1u) >> bsh], 1u);
-      }
-    }
-    for (uint32_t i0 = kSpecTail * kThreads; i0 < n_c; i0 += 4 * kThreads) {
-      uint32_t b4[4], x4[4];
+  if (bins) {  // count the outliers into key bins
+    for (int i = tid; i < kNB; i += kThreads) hc[i] = 0u;
+    tsync();
+    for (int i0 = 0; i0 < (int)n_c; i0 += 4 * kThreads) {
+      uint32_t b4[4];
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
-        const uint32_t i = i0 + tid + j * kThreads;
-        b4[j] = x4[j] = 0u;
-        if (i < n_c) { b4[j] = __ldcg(P.cand_bits + rb + i); x4[j] = __ldcg(P.cand_idx + rb + i); }
+        const int i = i0 + tid + j * kThreads;
+        b4[j] = i < (int)n_c ? xb[i] : 0u;
       }
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const uint32_t i = i0 + tid + j * kThreads;
-        if (i < n_c) {
-          xb[i] = b4[j]; xi[i] = x4[j];
-          if (bins) atomicAdd(&hc[(key_of_bits(b4[j]) - bl - 1u) >> bsh], 1u);
-        }
-      }
+      for (int j = 0; j < 4; ++j)
+        if (i0 + tid + j * kThreads < (int)n_c) atomicAdd(&hc[(key_of_bits(b4[j]) - bl - 1u) >> bsh], 1u);
     }
-    __syncthreads();
+    tsync();
   }
   QRITA_TSTAMP(2);
 
@@ -1201,7 +1242,7 @@ __device__ __forceinline__ void tail_body(const Params &P, uint8_t *dsmem, TailS
       run += c4[j];
     }
     if (tid == 0) { sm.bail = 0u; sm.L = k; }
-    __syncthreads();
+    tsync();
     QRITA_TSTAMP(10);
     const uint32_t bstar = sm.bstar;
     const uint32_t nC = sm.nabove + hc[bstar];
@@ -1215,7 +1256,7 @@ __device__ __forceinline__ void tail_body(const Params &P, uint8_t *dsmem, TailS
           cb[pos] = b; ci[pos] = xi[i];
         }
       }
-      __syncthreads();
+      tsync();
       QRITA_TSTAMP(11);
       // 3. order inside every bin by (key desc, index asc): rank against the bin's other entries
       for (int q = tid; q < (int)nC; q += kThreads) {
@@ -1230,7 +1271,7 @@ __device__ __forceinline__ void tail_body(const Params &P, uint8_t *dsmem, TailS
         }
         db[e - c + r] = b; di[e - c + r] = ix;
       }
-      __syncthreads();
+      tsync();
       QRITA_TSTAMP(12);
       if (sm.bail == 0u) {  // block-uniform
         uint32_t L = k;
@@ -1271,7 +1312,7 @@ __device__ __forceinline__ void tail_body(const Params &P, uint8_t *dsmem, TailS
               if (fx_ge(pre, pl.t_p)) { atomicMin(&sm.L, (uint32_t)q + 1u); break; }
             }
           }
-          __syncthreads();
+          tsync();
           // p >= fsum(all survivors): keep them all (oracle.py:45-46)
           L = fx_ge(Mtot, pl.t_sp) ? sm.L : k;
           met.p_search_iters = 1;
@@ -1286,7 +1327,7 @@ __device__ __forceinline__ void tail_body(const Params &P, uint8_t *dsmem, TailS
         sorted_out = true;
       }
     }
-    __syncthreads();
+    tsync();
   }
   QRITA_TSTAMP(3);
   const SrcX X{xb, xi, (int)n_c};
@@ -1342,7 +1383,7 @@ __device__ __forceinline__ void tail_body(const Params &P, uint8_t *dsmem, TailS
     if (!topp_only && k_used_x && n_s <= (uint32_t)kCapS) {
       // compact S into shared memory with its exp values (order is irrelevant: sums are exact)
       if (tid == 0) sm.u[4] = 0u;
-      __syncthreads();
+      tsync();
       for (int i0 = 0; i0 < X.n; i0 += kThreads) {
         const int i = i0 + tid;
         const uint32_t b = i < X.n ? xb[i] : 0u;
@@ -1350,14 +1391,14 @@ __device__ __forceinline__ void tail_body(const Params &P, uint8_t *dsmem, TailS
         const uint32_t pos = warp_reserve(&sm.u[4], in);
         if (in) { sb[pos] = b; si[pos] = xi[i]; sp[pos] = e_of(b); }
       }
-      __syncthreads();
+      tsync();
       ns_cached = sm.u[4];
-      __syncthreads();
+      tsync();
       const SrcX S{sb, si, (int)ns_cached};
       const Fx Dx = block_mass(S, [&](uint32_t, uint32_t, int i, double &v) { v = sp[i]; return true; }, cnt_dummy, red);
       D = fx_to_double(Dx);
       for (int i = tid; i < (int)ns_cached; i += kThreads) sp[i] = sp[i] / D;
-      __syncthreads();
+      tsync();
       s_cached = true;
     } else if (!topp_only && k_used_x) {
       const Fx Dx = block_mass(X, [&](uint32_t b, uint32_t ix, int, double &v) {
@@ -1434,9 +1475,9 @@ __device__ __forceinline__ void tail_body(const Params &P, uint8_t *dsmem, TailS
         while (j < pr.n_eq && !fx_ge(fx_add(pr.H, fx_mul_u32(fb, j)), Tp)) ++j;
         sm.u[5] = j;
       }
-      __syncthreads();
+      tsync();
       uint32_t j = sm.u[5];
-      __syncthreads();
+      tsync();
       if (nodup) j = pr.n_eq;
       Kf = pr.K;
       kept = pr.n_gt + j;
@@ -1472,6 +1513,64 @@ __device__ __forceinline__ void tail_body(const Params &P, uint8_t *dsmem, TailS
     if (P.kept_count) P.kept_count[row] = (int32_t)kept;
     if (P.metrics) P.metrics[row] = met;
   }
+}
+
+// Row tail of the staged pipeline: waits for qrita_stream, gathers the row's outliers from its HBM
+// row buffer into shared memory in one round trip, then resolves.
+template <typename T, int NP>
+__device__ __forceinline__ void tail_body(const Params &P, uint8_t *dsmem, TailSmem &sm) {
+  const int row = blockIdx.x;
+  pdl_wait();  // outliers and row aggregates of qrita_stream (and plans of qrita_prep)
+  QRITA_TSTAMP(0);
+  const int tid = threadIdx.x;
+  RowPlan pl;
+  {
+    const uint4 *src4 = reinterpret_cast<const uint4 *>(P.plans + row);
+    uint4 *dst4 = reinterpret_cast<uint4 *>(&pl);
+#pragma unroll
+    for (int i = 0; i < (int)(sizeof(RowPlan) / 16); ++i) dst4[i] = __ldcg(src4 + i);
+  }
+  uint32_t *xb = (uint32_t *)dsmem;      // [kCapX] outlier bits
+  uint32_t *xi = xb + kCapX;             // [kCapX] outlier indices
+  // one round trip: the row aggregate, and speculatively the first kSpecTail * kThreads outliers of
+  // the row buffer (coalesced; entries past the count are ignored)
+  const size_t rb = (size_t)row * P.xcap;
+  const uint4 a0 = __ldcg(reinterpret_cast<const uint4 *>(P.agg + row));
+  const uint4 a1 = __ldcg(reinterpret_cast<const uint4 *>(P.agg + row) + 1);
+  uint32_t vb[kSpecTail], vi[kSpecTail];
+#pragma unroll
+  for (int j = 0; j < kSpecTail; ++j) {
+    const int i = tid + j * kThreads;
+    vb[j] = vi[j] = 0u;
+    if (i < P.xcap) { vb[j] = __ldcg(P.cand_bits + rb + i); vi[j] = __ldcg(P.cand_idx + rb + i); }
+  }
+  const uint32_t n_c = a0.x;
+  const bool overflow = a1.x != 0u || n_c > (uint32_t)P.xcap;
+  if (pl.has_thr && !overflow && n_c <= (uint32_t)kCapX) {
+#pragma unroll
+    for (int j = 0; j < kSpecTail; ++j) {
+      const uint32_t i = (uint32_t)(tid + j * kThreads);
+      if (i < n_c) { xb[i] = vb[j]; xi[i] = vi[j]; }
+    }
+    for (uint32_t i0 = kSpecTail * kThreads; i0 < n_c; i0 += 4 * kThreads) {
+      uint32_t b4[4], x4[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const uint32_t i = i0 + tid + j * kThreads;
+        b4[j] = x4[j] = 0u;
+        if (i < n_c) { b4[j] = __ldcg(P.cand_bits + rb + i); x4[j] = __ldcg(P.cand_idx + rb + i); }
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const uint32_t i = i0 + tid + j * kThreads;
+        if (i < n_c) { xb[i] = b4[j]; xi[i] = x4[j]; }
+      }
+    }
+  }
+  tsync();
+  QRITA_TSTAMP(1);
+  tail_resolve<T, NP>(P, row, pl, xb, xi, dsmem + (size_t)kCapX * 8, sm, n_c, overflow, a0.y, a0.z, a0.w,
+                      (uint32_t)kCapX);
 }
 
 template <typename T, int NP>
@@ -1680,6 +1779,258 @@ __global__ void __launch_bounds__(kStreamThreads, 3) qrita_stream(Params P) {
   if (!waited) pdl_wait();
 }
 
+// ------------------------------------------------------------------------------------------------
+// Fused single-kernel pipeline: one CTA owns one row at a time
+// ------------------------------------------------------------------------------------------------
+// CTA = kThreads tail/consumer threads (8 warps) + 1 TMA producer warp; two CTAs per SM, persistent
+// over rows (row = blockIdx.x + i * gridDim.x).  Per row:
+//   producer  streams the row through a ring of kRing 4 KB shared-memory stages with bulk copies
+//             (cp.async.bulk, L2 evict_first) completing on per-stage mbarriers;
+//   consumers (1) compute the sigma plan from the first sample stages in place (compute_plan: the
+//             numpy pairwise statistics of sigma_trunc.py:69-103), (2) consume the chunks warp by
+//             warp: NaN-propagating row extrema, outliers (z >= threshold) appended straight into
+//             shared memory X with warp-aggregated slots, the -inf (or copy) background written to
+//             HBM with streaming 128-bit stores, (3) run tail_resolve on X with the ring reused as
+//             its work area.
+// The row never leaves the SM between reading and resolving: no outlier workspace, no inter-kernel
+// dependency, one launch per call.  The other CTA on the SM streams while this one resolves.
+// Shared memory per CTA (two CTAs per SM, <= 113 KB each): X = kCapXF outliers (48 KB; cfg2/cfg4 rows
+// peak at 4.8k / 5.8k) + a ring of kRing 4 KB stages (60 KB in flight per CTA, 120 KB per SM), which
+// doubles as the tail's work area once the row is consumed.
+constexpr int kStageBytes = 4096;
+constexpr int kCapXF = 6144;
+constexpr int kRing = 15;
+constexpr int kFusedThreads = kThreads + 32;
+static_assert(kRing >= 8, "ring must hold the sigma sample (<= 6 stages) plus slack");
+static_assert(kRing * kStageBytes >= kWorkBytes, "the ring doubles as the tail work area");
+static_assert(sizeof(PlanScratch) <= (size_t)kCapXF * 8, "plan scratch aliases the outlier area");
+
+struct FusedSmem {
+  TailSmem tail;
+  RowPlan pl;
+  unsigned long long full[kRing];   // stage filled (TMA transaction bytes)
+  unsigned long long empty[kRing];  // stage consumed (one consumer warp)
+  uint32_t seq[kRing];              // chunk sequence number last issued into the stage
+  uint32_t n_x;                     // outliers of the current row (all of them, even past kCapX)
+  uint32_t wmx[kWarps], wnf[kWarps];
+};
+
+// Wait until chunk g has landed in its stage.  Warps consume chunks round-robin, so a warp may ask for
+// use n of a stage before use n-1 has landed; a bare parity wait would then see the completed phase
+// n-2 and return early.  The producer records g in seq[] only after use n-1 was consumed, so once seq
+// shows g the barrier is in phase n (copy in flight) or n+1 (landed) and the parity is unambiguous.
+__device__ __forceinline__ void stage_wait(FusedSmem &fs, uint32_t g) {
+  const uint32_t slot = g % kRing;
+  while (*(volatile const uint32_t *)&fs.seq[slot] != g) {
+  }
+  mbar_wait(&fs.full[slot], (g / kRing) & 1u);
+}
+
+template <typename T>
+__device__ __forceinline__ float elem_f(T v) { return __uint_as_float(Elem<T>::bits(v)); }
+
+__device__ __forceinline__ float max3_nan(float a, float b, float c) {
+  float r;
+  asm("max.NaN.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+  return r;
+}
+__device__ __forceinline__ float max3f(float a, float b, float c) {
+  float r;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+  return r;
+}
+template <int N> struct MaskT { using type = uint32_t; };
+template <> struct MaskT<64> { using type = unsigned long long; };
+
+// One consumer warp, one chunk of CE = 4 KB / sizeof(T) elements staged in shared memory.  Per
+// element: a 3-input max (row max), a 3-input NaN-propagating max of |x| (non-finite detection), one
+// compare folded into a per-lane outlier bit mask.  Then one warp scan + one shared atomic reserve
+// the chunk's slots in X, and each lane copies its outliers (re-read from the stage by bit index).
+template <typename T>
+__device__ __forceinline__ void consume_chunk(const uint8_t *stage, int c0, int n, float thr, bool write_bg,
+                                              bool write_copy, T *dst, uint32_t *n_x, uint32_t *xb,
+                                              uint32_t *xi, float &rmx, float &ramx) {
+  using VT = typename Vec<T>::type;
+  constexpr int W = Vec<T>::W;
+  constexpr int CE = kStageBytes / (int)sizeof(T);
+  constexpr int U = CE / (32 * W);
+  using M = typename MaskT<U * W>::type;
+  const int lane = threadIdx.x & 31;
+  const T *st = reinterpret_cast<const T *>(stage);
+  M m = 0;
+  if (n == CE) {
+    const VT *sv = reinterpret_cast<const VT *>(stage);
+    VT v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) v[u] = sv[u * 32 + lane];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+#pragma unroll
+      for (int w = 0; w < W; w += 2) {
+        const float x0 = lane_f<T>(v[u], w), x1 = lane_f<T>(v[u], w + 1);
+        rmx = max3f(rmx, x0, x1);
+        ramx = max3_nan(ramx, fabsf(x0), fabsf(x1));
+        m |= (M)(x0 >= thr) << (u * W + w);
+        m |= (M)(x1 >= thr) << (u * W + w + 1);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int e = (u * 32 + lane) * W;
+      if (write_bg) __stcs(reinterpret_cast<VT *>(dst + e), neg_inf_vec<T>());
+      else if (write_copy) __stcs(reinterpret_cast<VT *>(dst + e), v[u]);
+    }
+  } else {  // ragged tail chunk of the row: element-wise, same (u, lane, w) layout
+    for (int u = 0; u < U; ++u) {
+      const int e = (u * 32 + lane) * W;
+#pragma unroll
+      for (int w = 0; w < W; ++w) {
+        if (e + w < n) {
+          const float x = elem_f<T>(st[e + w]);
+          rmx = fmaxf(rmx, x);
+          ramx = max_nan(ramx, fabsf(x));
+          m |= (M)(x >= thr) << (u * W + w);
+          if (write_bg || write_copy) dst[e + w] = write_bg ? Elem<T>::neg_inf() : st[e + w];
+        }
+      }
+    }
+  }
+  // reserve this warp's outlier slots in X (one shared atomic per chunk)
+  const uint32_t cnt = (uint32_t)__popcll((unsigned long long)m);
+  uint32_t incl = cnt;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += t;
+  }
+  const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+  if (total == 0u) return;
+  uint32_t base = 0u;
+  if (lane == 31) base = atomicAdd(n_x, total);
+  uint32_t pos = __shfl_sync(0xffffffffu, base, 31) + incl - cnt;
+  while (m) {
+    const int j = __ffsll((long long)m) - 1;
+    m &= m - 1;
+    const int e = ((j / W) * 32 + lane) * W + (j % W);
+    if (pos < (uint32_t)kCapXF) { xb[pos] = Elem<T>::bits(st[e]); xi[pos] = (uint32_t)(c0 + e); }
+    ++pos;
+  }
+}
+
+template <typename T, int NP>
+__global__ void __launch_bounds__(kFusedThreads, 2) qrita_fused(Params P) {
+  extern __shared__ __align__(128) uint8_t dsmem[];
+  __shared__ FusedSmem fs;
+  constexpr int CE = kStageBytes / (int)sizeof(T);
+  uint32_t *xb = (uint32_t *)dsmem;
+  uint32_t *xi = xb + kCapXF;
+  uint8_t *ring = dsmem + (size_t)kCapXF * 8;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int V = P.V;
+  const int nch = (V + CE - 1) / CE;
+  if (tid == 0) {
+    for (int i = 0; i < kRing; ++i) {
+      mbar_init(&fs.full[i], 1u);
+      mbar_init(&fs.empty[i], 1u);
+      fs.seq[i] = 0xffffffffu;
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+  uint32_t g0 = 0u;  // chunks of this CTA's earlier rows: stage sequence shared by producer and consumers
+  for (int row = blockIdx.x; row < P.B; row += gridDim.x) {
+    const T *in = (const T *)P.logits + (size_t)row * P.ld_in;
+    if (warp == kWarps) {
+      // ---------------- producer: the whole row through the ring ----------------
+      if (lane == 0) {
+        const unsigned long long pol = l2_evict_first_policy();
+        fence_proxy_async_smem();  // the previous row's tail wrote the ring through the generic proxy
+        for (int c = 0; c < nch; ++c) {
+          const uint32_t g = g0 + (uint32_t)c, slot = g % kRing;
+          mbar_wait(&fs.empty[slot], ((g / kRing) & 1u) ^ 1u);
+          *(volatile uint32_t *)&fs.seq[slot] = g;  // before the copy: consumers may wait on its parity
+          const uint32_t bytes = (uint32_t)(min(CE, V - c * CE) * (int)sizeof(T));
+          mbar_arrive_expect_tx(&fs.full[slot], bytes);
+          tma_load_1d(ring + (size_t)slot * kStageBytes, in + (size_t)c * CE, bytes, &fs.full[slot], pol);
+        }
+      }
+      __syncwarp();
+    } else {
+      // ---------------- consumers ----------------
+      QRITA_TSTAMP(0);
+      // (1) plan: the sample-independent part while the first stages land, then the sample in place
+      if (tid == 0) { fs.n_x = 0u; plan_begin(P, row, &fs.pl); }
+      const int ns = P.tree.n_leaves > 0 ? (P.tree.n + CE - 1) / CE : 0;
+      for (int j = 0; j < ns; ++j) stage_wait(fs, g0 + (uint32_t)j);
+      tsync();
+      plan_sample<T>(P, [&](int i) -> float {
+        const uint32_t g = g0 + (uint32_t)(i / CE);
+        return elem_f<T>(reinterpret_cast<const T *>(ring + (size_t)(g % kRing) * kStageBytes)[i % CE]);
+      }, in, *reinterpret_cast<PlanScratch *>(dsmem), &fs.pl);
+      tsync();
+      QRITA_TSTAMP(1);
+      const RowPlan pl = fs.pl;
+      const bool inplace = (P.flags & QRITA_INPLACE) != 0;
+      const int mode = pl.mode;
+      const float thr = pl.has_thr ? __uint_as_float(bits_of_key(pl.key_thr)) : __uint_as_float(0x7fffffffu);
+      const bool write_bg = !inplace && (mode == MODE_TOPK || mode == MODE_TOPKP || mode == MODE_INVALID);
+      const bool write_copy = !inplace && mode == MODE_PASS;
+      T *dst = (T *)P.out + (size_t)row * P.ld_out;
+      // (2) stream: warp w consumes chunks w, w + 8, ...
+      float rmx = -3.402823466e38f, ramx = 0.0f;  // row max; NaN-propagating max |x| (non-finite check)
+      for (int c = warp; c < nch; c += kWarps) {
+        const uint32_t g = g0 + (uint32_t)c, slot = g % kRing;
+        stage_wait(fs, g);
+        consume_chunk<T>(ring + (size_t)slot * kStageBytes, c * CE, min(CE, V - c * CE), thr, write_bg,
+                         write_copy, dst + (size_t)c * CE, &fs.n_x, xb, xi, rmx, ramx);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&fs.empty[slot]);
+      }
+      {
+        const uint32_t mx = warp_max(key_of_bits(__float_as_uint(rmx)));
+        const bool nf = __any_sync(0xffffffffu, !(ramx <= 3.402823466e38f));
+        if (lane == 0) { fs.wmx[warp] = mx; fs.wnf[warp] = nf ? 0u : 0xffffffffu; }
+      }
+      tsync();
+      QRITA_TSTAMP(2);
+      // minkey 0: the full-row fallback searches start below every finite key; a non-finite row
+      // reports column 0 and the error path locates the first bad column exactly
+      uint32_t maxkey = 0u, minkey = 0u, nf_col = 0xffffffffu;
+#pragma unroll
+      for (int w = 0; w < kWarps; ++w) {
+        maxkey = max(maxkey, fs.wmx[w]);
+        nf_col = min(nf_col, fs.wnf[w]);
+      }
+      // (3) resolve; every stage of this row has been consumed, so the ring is the work area
+      tail_resolve<T, NP>(P, row, pl, xb, xi, ring, fs.tail, fs.n_x, false, maxkey, minkey, nf_col,
+                          (uint32_t)kCapXF);
+    }
+    g0 += (uint32_t)nch;
+    __syncthreads();  // row done: the ring and X may be refilled
+  }
+}
+
+constexpr size_t kFusedDynSmem = (size_t)kCapXF * 8 + (size_t)kRing * kStageBytes;
+
+template <typename T, int NP>
+static cudaError_t launch_fused(const Params &P, cudaStream_t st) {
+  static int grid_cap = 0;  // per instantiation
+  if (grid_cap == 0) {
+    cudaError_t e = cudaFuncSetAttribute(qrita_fused<T, NP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)kFusedDynSmem);
+    if (e != cudaSuccess) return e;
+    int dev = 0, sms = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, qrita_fused<T, NP>, kFusedThreads, kFusedDynSmem);
+    if (e != cudaSuccess) return e;
+    grid_cap = sms * (per_sm < 1 ? 1 : per_sm);
+  }
+  const int grid = P.B < grid_cap ? P.B : grid_cap;
+  qrita_fused<T, NP><<<grid, kFusedThreads, kFusedDynSmem, st>>>(P);
+  return cudaGetLastError();
+}
+
 constexpr size_t kTailDynSmem = (size_t)kCapX * 8 + (size_t)kWorkBytes;
 
 template <typename T, int NP, bool VEC>
@@ -1740,6 +2091,14 @@ static cudaError_t launch_pipeline(const Params &P, cudaStream_t st, cudaEvent_t
 template <typename T>
 static cudaError_t launch_all(const Params &P, cudaStream_t st, bool vec, cudaEvent_t prep_done,
                               cudaEvent_t stream_done) {
+  // fused single-kernel path: rows and their tail ends must be 16-byte aligned for the bulk copies
+  const bool fused_ok = vec && ((size_t)P.V * sizeof(T)) % 16 == 0 && !(P.flags & QRITA_STAGED);
+  if (fused_ok) {
+    if (prep_done) cudaEventRecord(prep_done, st);
+    cudaError_t e = (P.flags & QRITA_SEARCH_BINARY) ? launch_fused<T, 1>(P, st) : launch_fused<T, 3>(P, st);
+    if (e == cudaSuccess && stream_done) e = cudaEventRecord(stream_done, st);
+    return e;
+  }
   if (P.flags & QRITA_SEARCH_BINARY)
     return vec ? launch_pipeline<T, 1, true>(P, st, prep_done, stream_done)
                : launch_pipeline<T, 1, false>(P, st, prep_done, stream_done);

@@ -30,6 +30,7 @@ class TruncFlags:
     force_fallback: bool = False
     dup_handling: bool = True
     debug_timing: bool = False          # record tail phase timestamps (qrita_get_timing)
+    staged: bool = False                # force the staged prep/stream/tail pipeline (ablation)
 
     def bits(self) -> int:
         if self.search not in ("quaternary", "binary"):
@@ -45,6 +46,8 @@ class TruncFlags:
             f |= N.NO_DUP
         if self.debug_timing:
             f |= N.DEBUG_TIMING
+        if self.staged:
+            f |= N.STAGED
         return f
 
 

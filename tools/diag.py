@@ -137,3 +137,37 @@ if len(sys.argv) > 1 and sys.argv[1] == "timing":
             d = np.where(ok, cur - prev, 0)
             print(f"     {nm:8s} mean {d[ok].mean()/1e3 if ok.any() else 0:7.2f} us  max {d.max()/1e3:7.2f}")
             prev = np.where(cur > 0, cur, prev)
+
+if len(sys.argv) > 1 and sys.argv[1] == "ftiming":
+    # fused kernel: per-row phases (0 row start, 1 plan, 2 streamed, 9 end) and the CTA timeline
+    import bench, ctypes
+    from paper_2602_01518_b200 import _native as N
+    for cfg in sys.argv[2:]:
+        x, k, p, dtype, desc = bench.workload(cfg)
+        tdt = torch.bfloat16 if dtype == "bf16" else torch.float32
+        xt = torch.from_numpy(x).cuda().to(tdt)
+        kt, pt = torch.from_numpy(k).cuda(), torch.from_numpy(p).cuda()
+        fl = Q.TruncFlags(debug_timing=True)
+        st = torch.cuda.current_stream()
+        ws = Q.ops.workspace_for(xt.device, st)
+        for _ in range(3):
+            Q.topk_topp(xt, kt, pt, flags=fl)
+        ptr, _ = ws.get(0, st)
+        B = x.shape[0]
+        ws.buf.zero_()
+        Q.topk_topp(xt, kt, pt, flags=fl)
+        buf = (ctypes.c_ulonglong * (16 * B))()
+        N.load().qrita_get_timing(ctypes.c_void_p(ptr), B, buf, ctypes.c_void_p(st.cuda_stream))
+        a = np.frombuffer(buf, dtype=np.uint64).reshape(B, 16).astype(np.int64)
+        t0 = a[:, 0].min()
+        end = np.where(a[:, 9] > 0, a[:, 9], a[:, 2])
+        print(f"{cfg}: B={B} start spread {(a[:,0].max()-t0)/1e3:.1f} us, last end {(end.max()-t0)/1e3:.1f} us")
+        for nm, i, j in (("plan", 0, 1), ("stream", 1, 2), ("resolve", 2, 9)):
+            ok = (a[:, i] > 0) & (a[:, j] > 0)
+            d = (a[ok, j] - a[ok, i]) / 1e3
+            if ok.any():
+                print(f"   {nm:8s} mean {d.mean():7.2f} us  min {d.min():7.2f}  max {d.max():7.2f}")
+        q = np.percentile((a[:, 0] - t0) / 1e3, [0, 25, 50, 75, 100])
+        print("   row start percentiles", np.round(q, 1))
+        q = np.percentile((end - t0) / 1e3, [0, 25, 50, 75, 100])
+        print("   row end percentiles  ", np.round(q, 1))
