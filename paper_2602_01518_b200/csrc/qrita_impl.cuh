@@ -167,6 +167,12 @@ __device__ double pairwise_tree(int n, LeafFn leaf) {
   }
 }
 
+// Smallest s with w <= kNB * 2^s: key bins (l, l + 2^s], (l + 2^s, l + 2^(s+1)], ... cover (l, l + w].
+__device__ __forceinline__ int bin_shift(uint32_t w) {
+  if (w <= (uint32_t)kNB) return 0;
+  return (32 - __clz(w - 1u)) - kLogNB;
+}
+
 // Row routing (pipeline.py:199-218): which stages run for (k, p).
 __device__ __forceinline__ int row_mode(int64_t k, double p, int V) {
   const bool bad_k = !(k >= 1 && k <= (int64_t)V);
@@ -225,7 +231,8 @@ __device__ __forceinline__ void plan_begin(const Params &P, int row, RowPlan *ou
     pl.t_sp = fx_zero();
   }
   pl.has_thr = want_thr ? 1 : 0;
-  pl.pad[0] = pl.pad[1] = pl.pad[2] = 0;
+  pl.bsh = 0;
+  pl.pad[0] = pl.pad[1] = 0;
   *out = pl;
   const bool bad_k = !(k >= 1 && k <= (int64_t)V);
   const bool bad_p = !(p > 0.0 && p <= 1.0);
@@ -258,6 +265,24 @@ __device__ void plan_sample(const Params &P, SampleAt xs, const T *a, PlanScratc
       }
     }
     tsync();
+    if (n == 4096 && nl == 32) {
+      // the default sample is a perfect tree: 32 leaves of 128 combined pairwise level by level
+      // (node = left + right), so one warp per sum finishes it with shuffles and no block barriers
+      if (tid < 64) {
+        const int sq = tid >> 5, L = tid & 31;
+        const double *r = sc.acc[sq][L];
+        double v = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                             __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const double u = __shfl_down_sync(0xffffffffu, v, o);
+          if ((L & (2 * o - 1)) == 0) v = __dadd_rn(v, u);
+        }
+        if (L == 0) sc.res[sq] = v;
+      }
+      tsync();
+      goto finish;
+    }
     for (int q = tid; q < nl * 2; q += kThreads) {
       const int L = q >> 1, sq = q & 1;
       const int o = tr.leaf_off[L], m = tr.leaf_len[L];
@@ -297,6 +322,7 @@ __device__ void plan_sample(const Params &P, SampleAt xs, const T *a, PlanScratc
         : pairwise_tree(n, [&](int o, int m) -> double { return leaf_sum<T, true>(a + o, m); });
   }
   tsync();
+finish:
   if (tid == 0) {
     const double sum = sc.res[0], sq = sc.res[1];
     // sigma_trunc.py:78-81 — mean, E[x^2] - mu^2 floored at 0, sqrt; no FMA contraction anywhere.
@@ -312,6 +338,11 @@ __device__ void plan_sample(const Params &P, SampleAt xs, const T *a, PlanScratc
     float f = __double2float_rd(t);
     if (!((double)f > t)) f = nextafterf(f, __uint_as_float(0x7f800000u));
     out->key_thr = key_of_bits(__float_as_uint(f));
+    // provisional outlier range (t, mu + 6 sigma] for bins counted while streaming; keys above it
+    // fall into the last (open) bin, so the binning stays monotone whatever the row holds
+    uint32_t khi = key_of_bits(__float_as_uint((float)__dadd_rn(mu, __dmul_rn(6.0, sigma))));
+    if (khi < out->key_thr) khi = out->key_thr;
+    out->bsh = bin_shift(khi - (out->key_thr - 1u));
     out->mu = mu;
     out->sigma = sigma;
     out->t = t;
@@ -431,11 +462,7 @@ __device__ __forceinline__ Fx block_exscan_fx(const Fx &v, Fx *buf, Fx &total) {
   return fx_sub(fx_add(before, incl), v);
 }
 
-// Smallest s with w <= kNB * 2^s: key bins (l, l + 2^s], (l + 2^s, l + 2^(s+1)], ... cover (l, l + w].
-__device__ __forceinline__ int bin_shift(uint32_t w) {
-  if (w <= (uint32_t)kNB) return 0;
-  return (32 - __clz(w - 1u)) - kLogNB;
-}
+
 
 constexpr int kBins = 256;  // buckets of the bracketing pass (== kThreads: one bucket per thread)
 
@@ -1140,7 +1167,9 @@ __device__ __forceinline__ void tail_stamp(const Params &P, int row, int i) {
 template <typename T, int NP>
 __device__ void tail_resolve(const Params &P, int row, const RowPlan &pl, uint32_t *xb, uint32_t *xi,
                              uint8_t *work, TailSmem &sm, uint32_t n_c, bool overflow, uint32_t maxkey,
-                             uint32_t minkey, uint32_t nf_col, uint32_t xcap) {
+                             uint32_t minkey, uint32_t nf_col, uint32_t xcap, const uint32_t *gxb = nullptr,
+                             const uint32_t *gxi = nullptr, uint32_t gcap = 0u,
+                             const uint32_t *hist_in = nullptr, int bsh_in = 0) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int V = P.V;
   const T *in = (const T *)P.logits + (size_t)row * P.ld_in;
@@ -1193,13 +1222,23 @@ __device__ void tail_resolve(const Params &P, int row, const RowPlan &pl, uint32
   const bool sigma = pl.has_thr != 0;
   const double m = value_of_key(maxkey);
   met.outlier_count = sigma ? (int32_t)n_c : 0;
+  // X = (xb, xi)[0, xcap) in shared memory, continued by (gxb, gxi)[0, gcap) in HBM (fused kernel)
   const bool x_fits = sigma && !overflow && n_c <= xcap;
+  const bool x_fits_all = sigma && !overflow && n_c <= xcap + gcap;
+  auto x_bits = [&](uint32_t i) -> uint32_t { return i < xcap ? xb[i] : __ldcg(gxb + (i - xcap)); };
+  auto x_idx = [&](uint32_t i) -> uint32_t { return i < xcap ? xi[i] : __ldcg(gxi + (i - xcap)); };
   // bin-sort resolve: sigma hit (count > k, sigma_trunc.py:127-133) of a top-k / top-k+top-p row
-  const bool bins = x_fits && NP == 3 && !force_fb && !nodup && (mode == MODE_TOPK || mode == MODE_TOPKP) &&
+  const bool bins = x_fits_all && NP == 3 && !force_fb && !nodup && (mode == MODE_TOPK || mode == MODE_TOPKP) &&
                     pl.k <= (int64_t)kCapC && n_c > (uint32_t)pl.k;
   const uint32_t bl = pl.key_thr ? pl.key_thr - 1u : 0u;  // every outlier key is > bl
-  const int bsh = bin_shift(maxkey - bl);
-  if (bins) {  // count the outliers into key bins
+  // key bins (bl + b*2^bsh, bl + (b+1)*2^bsh], the last one open above: monotone in the key
+  const int bsh = hist_in ? bsh_in : bin_shift(maxkey - bl);
+  auto bin_of = [&](uint32_t key) -> uint32_t {
+    const uint32_t b = (key - bl - 1u) >> bsh;
+    return b < (uint32_t)kNB ? b : (uint32_t)(kNB - 1);
+  };
+  const uint32_t *hcnt = hist_in ? hist_in : hc;
+  if (bins && !hist_in) {  // count the outliers into key bins (the fused kernel counts while streaming)
     for (int i = tid; i < kNB; i += kThreads) hc[i] = 0u;
     tsync();
     for (int i0 = 0; i0 < (int)n_c; i0 += 4 * kThreads) {
@@ -1207,11 +1246,11 @@ __device__ void tail_resolve(const Params &P, int row, const RowPlan &pl, uint32
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         const int i = i0 + tid + j * kThreads;
-        b4[j] = i < (int)n_c ? xb[i] : 0u;
+        b4[j] = i < (int)n_c ? x_bits((uint32_t)i) : 0u;
       }
 #pragma unroll
       for (int j = 0; j < 4; ++j)
-        if (i0 + tid + j * kThreads < (int)n_c) atomicAdd(&hc[(key_of_bits(b4[j]) - bl - 1u) >> bsh], 1u);
+        if (i0 + tid + j * kThreads < (int)n_c) atomicAdd(&hc[bin_of(key_of_bits(b4[j]))], 1u);
     }
     tsync();
   }
@@ -1228,10 +1267,14 @@ __device__ void tail_resolve(const Params &P, int row, const RowPlan &pl, uint32
   // shortest prefix of the top-k whose exactly-summed renormalised mass reaches p.
   if (bins) {
     const uint32_t k = (uint32_t)pl.k;
-    // 1. bin starts in descending order; the bin holding the k-th largest key
+    const bool topkp = mode == MODE_TOPKP;
+    // 1. bin starts in descending order; the bin holding the k-th largest key.  A bin takes part
+    //    (b >= b*) iff it starts before position k; one that is too large to order in place bails out
+    //    to the pivot search before anything is overwritten.
+    if (tid == 0) { sm.bail = 0u; sm.L = k; }
     uint32_t c4[4], loc = 0u;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) { c4[j] = hc[kNB - 1 - 4 * tid - j]; loc += c4[j]; }
+    for (int j = 0; j < 4; ++j) { c4[j] = hcnt[kNB - 1 - 4 * tid - j]; loc += c4[j]; }
     uint32_t tot;
     uint32_t run = block_exscan_u32(loc, sm.scan_u, tot);
 #pragma unroll
@@ -1239,66 +1282,93 @@ __device__ void tail_resolve(const Params &P, int row, const RowPlan &pl, uint32
       const int b = kNB - 1 - 4 * tid - j;
       he[b] = run;
       if (run < k && k <= run + c4[j]) { sm.bstar = (uint32_t)b; sm.nabove = run; }
+      if (run < k && c4[j] > (uint32_t)kMaxBin) sm.bail = 1u;
       run += c4[j];
     }
-    if (tid == 0) { sm.bail = 0u; sm.L = k; }
     tsync();
     QRITA_TSTAMP(10);
     const uint32_t bstar = sm.bstar;
-    const uint32_t nC = sm.nabove + hc[bstar];
-    if (nC <= (uint32_t)kCapC) {  // block-uniform
+    const uint32_t nC = sm.nabove + hcnt[bstar];
+    if (nC <= (uint32_t)kCapC && sm.bail == 0u) {  // block-uniform
       // 2. counting sort by bin (bins >= b*); order inside a bin is arbitrary so far
-      for (int i = tid; i < (int)n_c; i += kThreads) {
-        const uint32_t b = xb[i];
-        const uint32_t bin = (key_of_bits(b) - bl - 1u) >> bsh;
-        if (bin >= bstar) {
-          const uint32_t pos = atomicAdd(&he[bin], 1u);
-          cb[pos] = b; ci[pos] = xi[i];
+      for (int i0 = 0; i0 < (int)n_c; i0 += 4 * kThreads) {
+        uint32_t b4[4], p4[4];
+        bool in4[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int i = i0 + tid + j * kThreads;
+          b4[j] = i < (int)n_c ? x_bits((uint32_t)i) : 0u;
         }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const uint32_t bin = bin_of(key_of_bits(b4[j]));
+          in4[j] = i0 + tid + j * kThreads < (int)n_c && bin >= bstar;
+          p4[j] = in4[j] ? atomicAdd(&he[bin], 1u) : 0u;
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          if (in4[j]) { cb[p4[j]] = b4[j]; ci[p4[j]] = x_idx((uint32_t)(i0 + tid + j * kThreads)); }
       }
       tsync();
       QRITA_TSTAMP(11);
-      // 3. order inside every bin by (key desc, index asc): rank against the bin's other entries
+      // 3. order inside every bin by (key desc, index asc), ranking against the bin's other entries;
+      //    the k survivors' exp(z - max) go to ev (X is no longer needed) with per-warp exact partial
+      //    sums, so the normaliser needs no pass of its own
+      double *ev2 = reinterpret_cast<double *>(xb);
+      Fx se = fx_zero();
       for (int q = tid; q < (int)nC; q += kThreads) {
         const uint32_t b = cb[q], ix = ci[q], key = key_of_bits(b);
-        const uint32_t bin = (key - bl - 1u) >> bsh;
-        const uint32_t e = he[bin], c = hc[bin];
-        if (c > (uint32_t)kMaxBin) { sm.bail = 1u; continue; }
+        const uint32_t bin = bin_of(key);
+        const uint32_t e = he[bin], c = hcnt[bin];
         uint32_t r = 0u;
+#pragma unroll 4
         for (uint32_t j = e - c; j < e; ++j) {
           const uint32_t kj = key_of_bits(cb[j]);
           r += (kj > key || (kj == key && ci[j] < ix)) ? 1u : 0u;
         }
-        db[e - c + r] = b; di[e - c + r] = ix;
+        const uint32_t d = e - c + r;
+        db[d] = b; di[d] = ix;
+        if (topkp && d < k) {
+          const double ex = exp((double)__uint_as_float(b) - m);
+          ev2[d] = ex;
+          se = fx_add(se, fx_from_double(ex));
+        }
+      }
+      if (topkp) {
+        uint32_t pc[12];
+        fx_split(se, pc);
+#pragma unroll
+        for (int i = 0; i < 12; ++i) {
+          const uint32_t t = warp_sum(pc[i]);
+          if (lane == 0) sm.red[0][warp][i] = t;
+        }
       }
       tsync();
       QRITA_TSTAMP(12);
-      if (sm.bail == 0u) {  // block-uniform
+      {
         uint32_t L = k;
-        if (mode == MODE_TOPKP) {
-          // 4. normaliser over the k survivors (oracle.py:85-86): exact sum, rounded once
-          const int E = ((int)k + kThreads - 1) / kThreads;
-          const int q0 = tid * E;
-          Fx se = fx_zero();
-          for (int j = 0; j < E; ++j) {
-            const int q = q0 + j;
-            if (q < (int)k) {
-              const double e = exp((double)__uint_as_float(db[q]) - m);
-              ev[q] = e;
-              se = fx_add(se, fx_from_double(e));
-            }
+        if (topkp) {
+          // 4. normaliser over the k survivors (oracle.py:85-86): exact sum, rounded once.  Lane i < 12
+          //    totals piece i over the warps; the pieces are then broadcast within the warp.
+          uint32_t t = 0u;
+          if (lane < 12) {
+#pragma unroll
+            for (int w = 0; w < kWarps; ++w) t += sm.red[0][w][lane];
           }
-          Fx Dx;
-          (void)block_exscan_fx(se, sm.scan_f[0], Dx);
-          const double D = fx_to_double(Dx);
+          uint32_t pc[12];
+#pragma unroll
+          for (int i = 0; i < 12; ++i) pc[i] = __shfl_sync(0xffffffffu, t, i);
+          const double D = fx_to_double(fx_join(pc));
           QRITA_TSTAMP(13);
           // 5. exact prefix masses in sorted order; the first prefix whose fsum reaches p
+          const int E = ((int)k + kThreads - 1) / kThreads;
+          const int q0 = tid * E;
           Fx sp_loc = fx_zero();
           for (int j = 0; j < E; ++j) {
             const int q = q0 + j;
             if (q < (int)k) {
-              const double pi = ev[q] / D;
-              ev[q] = pi;
+              const double pi = ev2[q] / D;
+              ev2[q] = pi;
               sp_loc = fx_add(sp_loc, fx_from_double(pi));
             }
           }
@@ -1308,7 +1378,7 @@ __device__ void tail_resolve(const Params &P, int row, const RowPlan &pl, uint32
           for (int j = 0; j < E; ++j) {
             const int q = q0 + j;
             if (q < (int)k) {
-              pre = fx_add(pre, fx_from_double(ev[q]));
+              pre = fx_add(pre, fx_from_double(ev2[q]));
               if (fx_ge(pre, pl.t_p)) { atomicMin(&sm.L, (uint32_t)q + 1u); break; }
             }
           }
@@ -1794,11 +1864,12 @@ __global__ void __launch_bounds__(kStreamThreads, 3) qrita_stream(Params P) {
 //             its work area.
 // The row never leaves the SM between reading and resolving: no outlier workspace, no inter-kernel
 // dependency, one launch per call.  The other CTA on the SM streams while this one resolves.
-// Shared memory per CTA (two CTAs per SM, <= 113 KB each): X = kCapXF outliers (48 KB; cfg2/cfg4 rows
-// peak at 4.8k / 5.8k) + a ring of kRing 4 KB stages (60 KB in flight per CTA, 120 KB per SM), which
-// doubles as the tail's work area once the row is consumed.
+// Shared memory per CTA (two CTAs per SM, <= 113 KB each): X = kCapXF outliers (44 KB; further ones
+// spill to the row's HBM buffer) + a ring of kRing 4 KB stages (60 KB in flight per CTA, 120 KB per
+// SM), which doubles as the tail's work area once the row is consumed, + the outliers' key-bin
+// histogram (4 KB), counted while streaming.
 constexpr int kStageBytes = 4096;
-constexpr int kCapXF = 6144;
+constexpr int kCapXF = 5632;
 constexpr int kRing = 15;
 constexpr int kFusedThreads = kThreads + 32;
 static_assert(kRing >= 8, "ring must hold the sigma sample (<= 6 stages) plus slack");
@@ -1812,6 +1883,7 @@ struct FusedSmem {
   unsigned long long empty[kRing];  // stage consumed (one consumer warp)
   uint32_t seq[kRing];              // chunk sequence number last issued into the stage
   uint32_t n_x;                     // outliers of the current row (all of them, even past kCapX)
+  uint32_t hist[kNB];               // outliers per key bin (tail_resolve's bin sort)
   uint32_t wmx[kWarps], wnf[kWarps];
 };
 
@@ -1849,7 +1921,8 @@ template <> struct MaskT<64> { using type = unsigned long long; };
 template <typename T>
 __device__ __forceinline__ void consume_chunk(const uint8_t *stage, int c0, int n, float thr, bool write_bg,
                                               bool write_copy, T *dst, uint32_t *n_x, uint32_t *xb,
-                                              uint32_t *xi, float &rmx, float &ramx) {
+                                              uint32_t *xi, uint32_t *gxb, uint32_t *gxi, uint32_t gcap,
+                                              uint32_t *hist, uint32_t bl, int bsh, float &rmx, float &ramx) {
   using VT = typename Vec<T>::type;
   constexpr int W = Vec<T>::W;
   constexpr int CE = kStageBytes / (int)sizeof(T);
@@ -1912,7 +1985,14 @@ __device__ __forceinline__ void consume_chunk(const uint8_t *stage, int c0, int 
     const int j = __ffsll((long long)m) - 1;
     m &= m - 1;
     const int e = ((j / W) * 32 + lane) * W + (j % W);
-    if (pos < (uint32_t)kCapXF) { xb[pos] = Elem<T>::bits(st[e]); xi[pos] = (uint32_t)(c0 + e); }
+    const uint32_t bits = Elem<T>::bits(st[e]);
+    const uint32_t bin = (key_of_bits(bits) - bl - 1u) >> bsh;
+    atomicAdd(&hist[bin < (uint32_t)kNB ? bin : (uint32_t)(kNB - 1)], 1u);
+    if (pos < (uint32_t)kCapXF) {
+      xb[pos] = bits; xi[pos] = (uint32_t)(c0 + e);
+    } else if (pos - (uint32_t)kCapXF < gcap) {  // spill past shared memory into the row's HBM buffer
+      gxb[pos - kCapXF] = bits; gxi[pos - kCapXF] = (uint32_t)(c0 + e);
+    }
     ++pos;
   }
 }
@@ -1961,6 +2041,7 @@ __global__ void __launch_bounds__(kFusedThreads, 2) qrita_fused(Params P) {
       // (1) plan: the sample-independent part while the first stages land, then the sample in place
       if (tid == 0) { fs.n_x = 0u; plan_begin(P, row, &fs.pl); }
       const int ns = P.tree.n_leaves > 0 ? (P.tree.n + CE - 1) / CE : 0;
+      for (int i = tid; i < kNB; i += kThreads) fs.hist[i] = 0u;
       for (int j = 0; j < ns; ++j) stage_wait(fs, g0 + (uint32_t)j);
       tsync();
       plan_sample<T>(P, [&](int i) -> float {
@@ -1976,13 +2057,15 @@ __global__ void __launch_bounds__(kFusedThreads, 2) qrita_fused(Params P) {
       const bool write_bg = !inplace && (mode == MODE_TOPK || mode == MODE_TOPKP || mode == MODE_INVALID);
       const bool write_copy = !inplace && mode == MODE_PASS;
       T *dst = (T *)P.out + (size_t)row * P.ld_out;
+      uint32_t *gxb = P.cand_bits + (size_t)row * P.xcap, *gxi = P.cand_idx + (size_t)row * P.xcap;
       // (2) stream: warp w consumes chunks w, w + 8, ...
       float rmx = -3.402823466e38f, ramx = 0.0f;  // row max; NaN-propagating max |x| (non-finite check)
       for (int c = warp; c < nch; c += kWarps) {
         const uint32_t g = g0 + (uint32_t)c, slot = g % kRing;
         stage_wait(fs, g);
         consume_chunk<T>(ring + (size_t)slot * kStageBytes, c * CE, min(CE, V - c * CE), thr, write_bg,
-                         write_copy, dst + (size_t)c * CE, &fs.n_x, xb, xi, rmx, ramx);
+                         write_copy, dst + (size_t)c * CE, &fs.n_x, xb, xi, gxb, gxi, (uint32_t)P.xcap, fs.hist,
+                         pl.key_thr - 1u, pl.bsh, rmx, ramx);
         __syncwarp();
         if (lane == 0) mbar_arrive(&fs.empty[slot]);
       }
@@ -2003,7 +2086,7 @@ __global__ void __launch_bounds__(kFusedThreads, 2) qrita_fused(Params P) {
       }
       // (3) resolve; every stage of this row has been consumed, so the ring is the work area
       tail_resolve<T, NP>(P, row, pl, xb, xi, ring, fs.tail, fs.n_x, false, maxkey, minkey, nf_col,
-                          (uint32_t)kCapXF);
+                          (uint32_t)kCapXF, gxb, gxi, (uint32_t)P.xcap, fs.hist, pl.bsh);
     }
     g0 += (uint32_t)nch;
     __syncthreads();  // row done: the ring and X may be refilled

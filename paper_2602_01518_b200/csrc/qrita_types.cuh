@@ -52,7 +52,8 @@ struct alignas(16) RowPlan {
   Fx t_p;             // smallest exact mass whose fsum is >= p
   Fx t_sp;            // smallest exact mass whose fsum is >= succ(p), i.e. > p
   int32_t has_thr;    // 0: no outliers gathered for this row
-  int32_t pad[3];
+  int32_t bsh;        // key-bin shift of the fused kernel's streaming histogram (provisional range)
+  int32_t pad[2];
 };
 static_assert(sizeof(RowPlan) % 16 == 0, "RowPlan is copied with 16-byte loads");
 

@@ -182,3 +182,26 @@ def test_verify_batch_with_exact_sort(cuda_device):
     batch = Q.synth_batch("quantized", 16, 512, seed=3, g=8)
     targets = Q.TruncTargets(np.arange(1, 17) * 7, np.linspace(0.3, 0.99, 16))
     assert Q.verify_batch(batch, targets, Q.EngineConfig()) == []
+
+
+def test_outlier_spill_rows(cuda_device):
+    """Rows whose sigma outliers exceed the fused kernel's shared-memory X (5632 entries) spill the rest
+    to the row's HBM buffer and still take the bin-sort path; fp32 and bf16."""
+    rng = np.random.default_rng(7)
+    v = 262144
+    x = rng.normal(size=(4, v)).astype(np.float32)
+    ks, ps = [2000, 1500, 700, 1900], [0.9, 1.0, 0.8, 0.95]
+    out, kept, met = run(x, ks, ps)
+    assert max(m["outlier_count"] for m in met) > 5632
+    assert all(m["full_row_path"] == 0 for m in met)
+    for i in range(x.shape[0]):
+        keep = oracle_keep_row(x[i], ks[i], ps[i])
+        want = np.where(keep, x[i], -np.inf).astype(np.float32)
+        assert G.same_bits(out[i], want).all(), i
+        assert kept[i] == keep.sum()
+    xb = to_bf16_bits(x[:2])
+    xf = (xb.astype(np.uint32) << 16).view(np.float32)
+    out, kept, _ = run(xf, ks[:2], ps[:2], dtype=torch.bfloat16)
+    for i in range(2):
+        keep = oracle_keep_row(xf[i], ks[i], ps[i])
+        assert np.array_equal(~np.isneginf(out[i]), keep), i
