@@ -279,16 +279,22 @@ def main():
     stream_ms = statistics.mean(bb.elapsed_time(c) for _, bb, c, _ in prof)
     tail_ms = statistics.mean(c.elapsed_time(d) for _, _, c, d in prof)
 
-    # roofline of the dominant kernel (qrita_stream: 1 read + 1 write of the [B, V] matrix)
+    # roofline of the dominant kernel: qrita_fused (one launch per step) reads and writes the [B, V]
+    # matrix once; its time is the e1 -> e2 interval of the profiling iterations above
+    kind = Q.ops.pipeline_kind(x)
     alg_bytes = b * v * esize * 2
     achieved = alg_bytes / (stream_ms / 1e3) / 1e9
     peak, peak_kind = measured_peak()
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": ncu_traffic(args.config),
-                "peak_source": peak_kind, "kernel": "qrita_stream",
-                "kernel_ms": stream_ms, "prep_ms": prep_ms, "tail_ms_serialised": tail_ms,
-                "alg_bytes_per_launch": alg_bytes,
+                "peak_source": peak_kind,
+                "kernel": "qrita_fused" if kind == "fused" else "qrita_stream",
+                "kernel_ms": stream_ms, "alg_bytes_per_launch": alg_bytes,
+                "alg_bytes_note": "B*V*sizeof(dtype) read + the same written (SURVEY.md 8d)",
                 "step_frac": alg_bytes / (ms_per_step / 1e3) / 1e9 / peak}
+    if kind == "staged":
+        roofline.update({"prep_ms": prep_ms, "tail_ms_serialised": tail_ms})
+    launches_per_step = 1 if kind == "fused" else 3
 
     line = {
         "metric": METRIC, "value": value, "unit": "rows/s", "n_gpus": world, "steps": args.steps,
@@ -300,7 +306,8 @@ def main():
         "hbm_gbs": alg_bytes / (ms_per_step / 1e3) / 1e9,
         "roofline": roofline,
         "clocks": clk.summary(),
-        "gpu_launches": 2 * args.steps,
+        "gpu_launches": launches_per_step * args.steps,
+        "pipeline": kind,
     }
 
     if not args.no_extras:
@@ -320,35 +327,32 @@ def main():
         line["torch_sort_baseline"] = {"value": sort_val, "unit": "rows/s",
                                        "ms_per_step": statistics.mean(ts), "exact": False,
                                        "ours_over_sort": value / world / sort_val}
-        # e2e through the public API: pinned host input -> device -> truncate (status-checked)
-        # -> pinned host output, copies inside the timed region
+        # e2e through the public API with HOST buffers: Q.topk_topp on pinned host tensors copies row
+        # chunks in, truncates and copies them back with both transfer directions overlapped with the
+        # kernels (ops.topk_topp_host); status-checked; the copies are inside the timed region
         x_host = torch.from_numpy(x_np).to(tdt).pin_memory()
-        k_host, p_host = torch.from_numpy(k_np).pin_memory(), torch.from_numpy(p_np).pin_memory()
+        k_host, p_host = torch.from_numpy(k_np), torch.from_numpy(p_np)
         o_host = torch.empty_like(x_host).pin_memory()
-        xd, kd, pd = torch.empty_like(x), torch.empty_like(k), torch.empty_like(p)
         e2e_steps = max(3, min(args.steps, 10))
         tt = []
         for i in range(e2e_steps + 2):
             torch.cuda.synchronize(dev)
             e0.record(st)
-            xd.copy_(x_host, non_blocking=True)
-            kd.copy_(k_host, non_blocking=True)
-            pd.copy_(p_host, non_blocking=True)
-            o = Q.topk_topp(xd, kd, pd, check=True)
-            o_host.copy_(o, non_blocking=True)
+            Q.topk_topp(x_host, k_host, p_host, out=o_host, check=True)
             e1.record(st)
             torch.cuda.synchronize(dev)
             if i >= 2:
                 tt.append(e0.elapsed_time(e1))
         h2d = x_host.numel() * x_host.element_size() + b * 16
-        d2h = o_host.numel() * o_host.element_size() + b * 8
+        d2h = o_host.numel() * o_host.element_size() + b * 4
         e2e_val = b / (statistics.mean(tt) / 1e3)
         if world > 1:
             t = torch.tensor([statistics.mean(tt)], dtype=torch.float64, device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e2e_val = world * b / (float(t.item()) / 1e3)
         line["e2e"] = {"value": e2e_val, "unit": "rows/s", "h2d_bytes_per_step": h2d,
-                       "d2h_bytes_per_step": d2h, "ms_per_step": statistics.mean(tt)}
+                       "d2h_bytes_per_step": d2h, "ms_per_step": statistics.mean(tt),
+                       "api": "paper_2602_01518_b200.topk_topp(pinned host tensors)"}
         if rank == 0 and world == 1 and not args.no_cpu_baseline:
             rows = b
             procs = min(os.cpu_count() or 1, rows)

@@ -148,7 +148,11 @@ def topk_topp(logits: torch.Tensor, k: Union[int, torch.Tensor], p: Union[float,
               check: bool = True, stream: Optional[torch.cuda.Stream] = None,
               prep_event: Optional[torch.cuda.Event] = None,
               stream_event: Optional[torch.cuda.Event] = None) -> torch.Tensor:
-    """Exact Top-k then Top-p truncation of a [B, V] CUDA tensor (fp32 or bf16).
+    """Exact Top-k then Top-p truncation of a [B, V] tensor (fp32 or bf16) on the GPU.
+
+    CUDA tensors are truncated in place on their device (stream-ordered).  Host tensors go through
+    topk_topp_host: row chunks are copied in, truncated and copied back with the transfers of both
+    directions overlapped with the kernels (the result is a host tensor).
 
     k: int64 per row (k == V disables top-k); p: float64 per row (p == 1 disables top-p).  Returns
     the masked logits (new tensor, or `logits` itself when inplace).  kept_count (int32 [B]) and
@@ -157,8 +161,13 @@ def topk_topp(logits: torch.Tensor, k: Union[int, torch.Tensor], p: Union[float,
     prep_event / stream_event (profiling only) are recorded after the preparation / streaming kernel;
     either one serialises the launches around it so the kernels can be timed alone.
     """
-    if not isinstance(logits, torch.Tensor) or not logits.is_cuda:
-        raise TypeError("logits must be a CUDA tensor (there is no CPU path)")
+    if isinstance(logits, torch.Tensor) and not logits.is_cuda:
+        if inplace or prep_event is not None or stream_event is not None:
+            raise ValueError("host tensors support neither inplace nor profiling events")
+        return topk_topp_host(logits, k, p, out=out, flags=flags, sample_size=sample_size,
+                              kept_count=kept_count, metrics=metrics, check=check)
+    if not isinstance(logits, torch.Tensor):
+        raise TypeError("logits must be a torch tensor")
     if logits.dim() != 2:
         raise ValueError("logit batch must be 2-D (rows x vocab)")
     if logits.dtype not in _DTYPES:
@@ -209,6 +218,18 @@ def topk_topp(logits: torch.Tensor, k: Union[int, torch.Tensor], p: Union[float,
     return out
 
 
+def pipeline_kind(logits: torch.Tensor, flags: Optional[TruncFlags] = None) -> str:
+    """Which kernel pipeline qrita_topk_topp runs for this tensor (mirrors the dispatch in
+    csrc/qrita_impl.cuh launch_all): "fused" (one launch: qrita_fused) when rows are 16-byte aligned
+    for the bulk copies, else "staged" (qrita_prep -> qrita_stream -> qrita_tail)."""
+    es = logits.element_size()
+    v = logits.shape[1]
+    ld = _row_stride(logits)
+    aligned = logits.data_ptr() % 16 == 0 and (ld * es) % 16 == 0 and (v * es) % 16 == 0
+    staged = flags is not None and flags.staged
+    return "fused" if aligned and not staged else "staged"
+
+
 def metrics_buffer(b: int, device) -> torch.Tensor:
     return torch.zeros((b, N.METRICS_BYTES), dtype=torch.uint8, device=device)
 
@@ -222,3 +243,97 @@ def decode_metrics(buf: torch.Tensor):
         m = N.RowMetricsC.from_buffer_copy(raw[i * sz:(i + 1) * sz])
         rows.append({f: getattr(m, f) for f, _ in N.RowMetricsC._fields_})
     return rows
+
+
+# ------------------------------------------------------------------------------------------------
+# Host buffers: chunked, overlapped transfers
+# ------------------------------------------------------------------------------------------------
+_host_lock = threading.Lock()
+_host_streams = {}
+
+
+def _streams_for(device: torch.device, n: int):
+    key = (device.index, n)
+    with _host_lock:
+        ss = _host_streams.get(key)
+        if ss is None:
+            ss = [torch.cuda.Stream(device) for _ in range(n)]
+            _host_streams[key] = ss
+        return ss
+
+
+def _status_view(ws: Workspace, b: int) -> torch.Tensor:
+    """The [status[b] | nf_col[b]] words at the head of a workspace (include/qrita_b200.h layout)."""
+    base = ws.buf.data_ptr()
+    off = ((base + 255) & ~255) - base
+    nf_off = off + ((4 * b + 255) // 256) * 256
+    st = ws.buf[off:off + 4 * b].view(torch.int32)
+    nf = ws.buf[nf_off:nf_off + 4 * b].view(torch.int32)
+    return st, nf
+
+
+def topk_topp_host(logits: torch.Tensor, k, p, *, out: Optional[torch.Tensor] = None,
+                   flags: Optional[TruncFlags] = None, sample_size: int = DEFAULT_SAMPLE_SIZE,
+                   kept_count: Optional[torch.Tensor] = None, metrics: Optional[torch.Tensor] = None,
+                   check: bool = True, device=None, chunk_bytes: int = 8 << 20,
+                   n_streams: int = 3) -> torch.Tensor:
+    """topk_topp for a host [B, V] tensor: rows go to the GPU in chunks of ~chunk_bytes round-robin
+    over n_streams streams; on each stream a chunk is copied in, truncated, and copied back, so the
+    host-to-device and device-to-host transfers of different chunks overlap each other and the
+    kernels.  Pinned host memory gives asynchronous copies; pageable memory works, synchronously.
+    Returns the masked logits as a host tensor (`out` when given).  kept_count / metrics, if given,
+    are CUDA tensors.  check=True raises the reference's ValueError for invalid rows (after all
+    chunks ran); the call always returns with the result in host memory."""
+    if logits.dim() != 2:
+        raise ValueError("logit batch must be 2-D (rows x vocab)")
+    if logits.dtype not in _DTYPES:
+        raise TypeError(f"unsupported dtype {logits.dtype}; expected float32 or bfloat16")
+    logits = logits.contiguous()
+    b, v = logits.shape
+    if b == 0 or v == 0:
+        raise ValueError("batch_size and vocab_size must be >= 1")
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    if out is None:
+        out = torch.empty_like(logits, pin_memory=logits.is_pinned())
+    elif out.shape != logits.shape or out.dtype != logits.dtype or out.is_cuda or not out.is_contiguous():
+        raise ValueError("out must be a contiguous host tensor matching logits")
+    kt = _per_row(k, b, torch.int64, dev, "k")
+    pt = _per_row(p, b, torch.float64, dev, "p")
+    rows = max(1, min(b, chunk_bytes // (v * logits.element_size())))
+    streams = _streams_for(dev, n_streams)
+    cur = torch.cuda.current_stream(dev)
+    status = torch.zeros((b,), dtype=torch.int32, device=dev)
+    nfcol = torch.full((b,), -1, dtype=torch.int32, device=dev)
+    with torch.cuda.device(dev):
+        for s in streams:
+            s.wait_stream(cur)  # k / p / status were produced on the current stream
+        bufs = {}
+        for i, r0 in enumerate(range(0, b, rows)):
+            r1 = min(b, r0 + rows)
+            s = streams[i % n_streams]
+            with torch.cuda.stream(s):
+                if s not in bufs:
+                    bufs[s] = (torch.empty((rows, v), dtype=logits.dtype, device=dev),
+                               torch.empty((rows, v), dtype=logits.dtype, device=dev))
+                xd, od = bufs[s]
+                xd, od = xd[:r1 - r0], od[:r1 - r0]
+                xd.copy_(logits[r0:r1], non_blocking=True)
+                topk_topp(xd, kt[r0:r1], pt[r0:r1], out=od, flags=flags, sample_size=sample_size,
+                          kept_count=kept_count[r0:r1] if kept_count is not None else None,
+                          metrics=metrics[r0:r1] if metrics is not None else None,
+                          check=False, stream=s)
+                st, nf = _status_view(workspace_for(dev, s), r1 - r0)
+                status[r0:r1].copy_(st, non_blocking=True)
+                nfcol[r0:r1].copy_(nf, non_blocking=True)
+                out[r0:r1].copy_(od, non_blocking=True)
+                for t in (xd, od):
+                    t.record_stream(s)
+        for s in streams:
+            cur.wait_stream(s)
+        if check:
+            bad = status.ne(0)
+            if bool(bad.any()):  # synchronises
+                raise TruncationError("invalid batch: " + "; ".join(
+                    describe_invalid(logits, kt.cpu(), pt.cpu())[:5] or ["invalid rows"]))
+        torch.cuda.synchronize(dev)
+    return out

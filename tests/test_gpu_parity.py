@@ -205,3 +205,19 @@ def test_outlier_spill_rows(cuda_device):
     for i in range(2):
         keep = oracle_keep_row(xf[i], ks[i], ps[i])
         assert np.array_equal(~np.isneginf(out[i]), keep), i
+
+
+def test_host_tensor_path(cuda_device):
+    """Host tensors in, host tensors out: chunked transfers overlapped over several streams
+    (ops.topk_topp_host); per-chunk status is gathered so errors still name the global row."""
+    x, k, p, dtype, trip, _ = G.config("cfg2")
+    n = 40  # 8 MB chunks of 16 rows -> 3 chunks over 3 streams
+    xh = torch.from_numpy(np.ascontiguousarray(x[:n])).pin_memory()
+    kept = torch.zeros(n, dtype=torch.int32, device="cuda")
+    out = Q.topk_topp(xh, torch.from_numpy(k[:n]), torch.from_numpy(p[:n]), kept_count=kept)
+    assert not out.is_cuda
+    assert_rows(x[:n], out.numpy(), kept.cpu().numpy(), trip[:n], "host path")
+    bad = xh.clone()
+    bad[20, 5] = float("nan")
+    with pytest.raises(ValueError, match="NaN logit at row 20, col 5"):
+        Q.topk_topp(bad, torch.from_numpy(k[:n]), torch.from_numpy(p[:n]))
