@@ -94,6 +94,33 @@ template <> struct Elem<uint16_t> {  // bf16 carried as raw bits; upcast to fp32
   static __device__ __forceinline__ uint16_t from_bits(uint32_t b) { return (uint16_t)(b >> 16); }
 };
 
+// 128-bit vectors of a dtype and their lanes as fp32 bit patterns
+template <typename T> struct Vec;
+template <> struct Vec<float> { using type = float4; static constexpr int W = 4; };
+template <> struct Vec<uint16_t> { using type = uint4; static constexpr int W = 8; };
+
+template <typename T>
+__device__ __forceinline__ uint32_t lane_bits(const typename Vec<T>::type &v, int w);
+template <>
+__device__ __forceinline__ uint32_t lane_bits<float>(const float4 &v, int w) {
+  return __float_as_uint(w == 0 ? v.x : w == 1 ? v.y : w == 2 ? v.z : v.w);
+}
+template <>
+__device__ __forceinline__ uint32_t lane_bits<uint16_t>(const uint4 &v, int w) {
+  const uint32_t x = (w >> 1) == 0 ? v.x : (w >> 1) == 1 ? v.y : (w >> 1) == 2 ? v.z : v.w;
+  return (w & 1) ? (x & 0xffff0000u) : (x << 16);
+}
+
+template <typename T>
+__device__ __forceinline__ typename Vec<T>::type neg_inf_vec();
+template <> __device__ __forceinline__ float4 neg_inf_vec<float>() {
+  const float n = __uint_as_float(0xff800000u);
+  return make_float4(n, n, n, n);
+}
+template <> __device__ __forceinline__ uint4 neg_inf_vec<uint16_t>() {
+  return make_uint4(0xff80ff80u, 0xff80ff80u, 0xff80ff80u, 0xff80ff80u);
+}
+
 // ------------------------------------------------------------------------------------------------
 // K0: per-row preparation (sigma_trunc.py:69-103; mode routing of pipeline.py:199-218)
 // ------------------------------------------------------------------------------------------------
@@ -172,6 +199,16 @@ __device__ __forceinline__ int bin_shift(uint32_t w) {
   if (w <= (uint32_t)kNB) return 0;
   return (32 - __clz(w - 1u)) - kLogNB;
 }
+
+// Debug phase timestamps of the row tail (QRITA_DEBUG_TIMING): P.dbg[row][i] = %globaltimer.
+__device__ __forceinline__ void tail_stamp(const Params &P, int row, int i) {
+  if ((P.flags & QRITA_DEBUG_TIMING) && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    P.dbg[(size_t)row * 16 + i] = t;
+  }
+}
+#define QRITA_TSTAMP(i) tail_stamp(P, row, (i))
 
 // Row routing (pipeline.py:199-218): which stages run for (k, p).
 __device__ __forceinline__ int row_mode(int64_t k, double p, int V) {
@@ -411,6 +448,9 @@ struct TailSmem {
   uint32_t scan_u[kWarps];      // bin sort: warp totals of the bin-start scan
   Fx scan_f[2][kWarps];         // bin sort: warp totals of the two mass scans
   uint32_t bstar, nabove, bail, L;
+  uint32_t nd, dabort, dK, dngt, dneq, dkmin, dkmax;  // distinct-value top-p
+  uint32_t scan_u2[kWarps];
+  Fx dH, dMx;
   SearchState st;
 };
 
@@ -1120,6 +1160,289 @@ __device__ uint32_t select_nth_eq(const Src &src, uint32_t K, uint32_t c, Red &R
   return res;
 }
 
+// Visits every element of a row in global memory, fn(i, valid, bits) with fp32-expanded bits, called by
+// all lanes (warp-converged, for match_any aggregation).  16-byte vector loads, kLd in flight per
+// thread, when the row is aligned.
+template <typename T, class Fn>
+__device__ __forceinline__ void for_row_warp(const T *in, int V, Fn fn) {
+  using VT = typename Vec<T>::type;
+  constexpr int W = Vec<T>::W;
+  const int tid = threadIdx.x;
+  if (((uintptr_t)in % 16) == 0 && V % W == 0) {
+    const VT *p = reinterpret_cast<const VT *>(in);
+    const int nv = V / W;
+    for (int b0 = 0; b0 < nv; b0 += kThreads * kLd) {
+      VT r[kLd];
+#pragma unroll
+      for (int j = 0; j < kLd; ++j) {
+        const int vi = b0 + j * kThreads + tid;
+        if (vi < nv) r[j] = __ldcg(p + vi);
+      }
+#pragma unroll
+      for (int j = 0; j < kLd; ++j) {
+        const int vi = b0 + j * kThreads + tid;
+#pragma unroll
+        for (int w = 0; w < W; ++w) fn(vi * W + w, vi < nv, vi < nv ? lane_bits<T>(r[j], w) : 0u);
+      }
+    }
+  } else {
+    for (int b0 = 0; b0 < V; b0 += kThreads * kLd) {
+      uint32_t r[kLd];
+#pragma unroll
+      for (int j = 0; j < kLd; ++j) {
+        const int i = b0 + j * kThreads + tid;
+        r[j] = i < V ? Elem<T>::bits(in[i]) : 0u;
+      }
+#pragma unroll
+      for (int j = 0; j < kLd; ++j) fn(b0 + j * kThreads + tid, b0 + j * kThreads + tid < V, r[j]);
+    }
+  }
+}
+
+struct DistinctRes {
+  bool ok;        // false: too many distinct values, use the pivot search
+  bool keep_all;  // p >= fsum(all)
+  uint32_t K, n_gt, n_eq, j;  // boundary key, entries above it, copies of it, copies kept
+  double mx;      // outlier mass (sigma_trunc.py:121), for the hit metric
+  bool hit;       // outlier mass > p
+};
+
+// Top-p over a whole row through its distinct values (pipeline.py:161-196 semantics of oracle.py:37-67).
+// Equal logits have equal probabilities, so the nucleus only needs each distinct value's count: one
+// pass counts them into a shared-memory hash table (warp-aggregated with match_any), then the
+// distinct values are sorted descending (bin counting sort) and fp64 exp, the exact normaliser
+// D = sum count * exp(v - m), probabilities fl(e / D) and the exact prefix masses are computed per
+// distinct value.  Rows with few distinct values (bf16 / quantised logits) cost one row pass instead
+// of a pivot search with an fp64 exp per element per pass.  tk/tc: table of cap (power of two)
+// entries; lk/lc, sk/sc: kCapC-entry lists; hc/he: kNB bins; ev: kCapC doubles.
+template <typename T>
+__device__ DistinctRes distinct_topp(const Params &P, int row, const T *in, int V, double m, const RowPlan &pl, uint32_t *tk,
+                                     uint32_t *tc, uint32_t cap, uint32_t *lk, uint32_t *lc, uint32_t *sk,
+                                     uint32_t *sc, uint32_t *hc, uint32_t *he, double *ev, TailSmem &sm) {
+  // lk/lc: compacted table, then the sorted result; sk/sc: grouped by bin
+  const int tid = threadIdx.x, lane = tid & 31;
+  const uint32_t lg = 31u - (uint32_t)__clz((int)cap);
+  const uint32_t limit = min(cap / 2u, (uint32_t)kCapC);
+  DistinctRes res{};
+  for (uint32_t h = tid; h < cap; h += kThreads) { tk[h] = 0u; tc[h] = 0u; }
+  for (int i = tid; i < kNB; i += kThreads) hc[i] = 0u;
+  if (tid == 0) { sm.nd = 0u; sm.dabort = 0u; sm.u[4] = 0u; sm.dkmin = 0xffffffffu; sm.dkmax = 0u; }
+  tsync();
+  // 1. count every distinct key (keys of finite logits are >= 1; 0 marks an empty slot)
+  for_row_warp<T>(in, V, [&](int, bool valid, uint32_t bits) {
+    const uint32_t key = valid ? key_of_bits(bits) : 0u;
+    const uint32_t peers = __match_any_sync(0xffffffffu, key);
+    if (!valid || lane != __ffs((int)peers) - 1 || sm.dabort) return;
+    const uint32_t n = (uint32_t)__popc(peers);
+    uint32_t h = (key * 0x9E3779B1u) >> (32u - lg);
+    for (uint32_t probe = 0; probe < cap; ++probe) {
+      const uint32_t cur = *(volatile uint32_t *)&tk[h];
+      if (cur == key) { atomicAdd(&tc[h], n); break; }
+      if (cur != 0u) { h = (h + 1u) & (cap - 1u); continue; }
+      const uint32_t old = atomicCAS(&tk[h], 0u, key);
+      if (old == 0u || old == key) {
+        atomicAdd(&tc[h], n);
+        if (old == 0u && atomicAdd(&sm.nd, 1u) >= limit) sm.dabort = 1u;
+        break;
+      }
+      h = (h + 1u) & (cap - 1u);
+    }
+  });
+  tsync();
+  QRITA_TSTAMP(10);
+  if (sm.dabort) return res;  // block-uniform
+  const uint32_t nd = sm.nd;
+  // 2. compact the table; key range of the distinct values
+  uint32_t kmin = 0xffffffffu, kmax = 0u;
+  for (uint32_t h0 = 0; h0 < cap; h0 += kThreads) {
+    const uint32_t h = h0 + tid;
+    const uint32_t key = h < cap ? tk[h] : 0u;
+    const bool keep = key != 0u;
+    const uint32_t pos = warp_reserve(&sm.u[4], keep);
+    if (keep) { lk[pos] = key; lc[pos] = tc[h]; kmin = min(kmin, key); kmax = max(kmax, key); }
+  }
+  kmin = warp_min(kmin);
+  kmax = warp_max(kmax);
+  if (lane == 0) { atomicMin(&sm.dkmin, kmin); atomicMax(&sm.dkmax, kmax); }
+  tsync();
+  kmin = sm.dkmin;
+  kmax = sm.dkmax;
+  // 3. sort descending: counting sort over key bins, then rank inside each bin (keys are distinct)
+  const int sh = bin_shift(kmax - kmin + 1u);
+  auto bin_of = [&](uint32_t key) -> uint32_t { return (key - kmin) >> sh; };
+  for (uint32_t i = tid; i < nd; i += kThreads) atomicAdd(&hc[bin_of(lk[i])], 1u);
+  tsync();
+  {
+    uint32_t c4[4], loc = 0u;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) { c4[j] = hc[kNB - 1 - 4 * tid - j]; loc += c4[j]; }
+    uint32_t tot;
+    uint32_t run = block_exscan_u32(loc, sm.scan_u, tot);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) { he[kNB - 1 - 4 * tid - j] = run; run += c4[j]; }
+  }
+  tsync();
+  for (uint32_t i = tid; i < nd; i += kThreads) {  // group by bin (order inside a bin arbitrary)
+    const uint32_t key = lk[i];
+    const uint32_t pos = atomicAdd(&he[bin_of(key)], 1u);
+    sk[pos] = key;
+    sc[pos] = lc[i];
+  }
+  tsync();
+  for (uint32_t q = tid; q < nd; q += kThreads) {  // rank inside the bin: he[b] is now the bin's end
+    const uint32_t key = sk[q], b = bin_of(key);
+    const uint32_t e = he[b], c = hc[b];
+    uint32_t r = 0u;
+    for (uint32_t j = e - c; j < e; ++j) r += sk[j] > key ? 1u : 0u;
+    lk[e - c + r] = key;
+    lc[e - c + r] = sc[q];
+  }
+  tsync();
+  // sorted: (lk, lc)[0, nd) by key descending
+  sk = lk;
+  sc = lc;
+  QRITA_TSTAMP(11);
+  // 4. exact normaliser and prefix masses over the sorted distinct values (thread t owns a
+  //    contiguous run of E entries)
+  const int E = ((int)nd + kThreads - 1) / kThreads;
+  const int q0 = tid * E;
+  Fx dl = fx_zero();
+  uint32_t cl = 0u;
+  for (int j = 0; j < E; ++j) {
+    const int q = q0 + j;
+    if (q < (int)nd) {
+      const double e = exp(value_of_key(sk[q]) - m);
+      ev[q] = e;
+      dl = fx_add(dl, fx_mul_u32(fx_from_double(e), sc[q]));
+      cl += sc[q];
+    }
+  }
+  Fx Dx;
+  (void)block_exscan_fx(dl, sm.scan_f[0], Dx);
+  const double D = fx_to_double(Dx);
+  Fx ml = fx_zero();
+  for (int j = 0; j < E; ++j) {
+    const int q = q0 + j;
+    if (q < (int)nd) {
+      const double pi = ev[q] / D;
+      ev[q] = pi;
+      ml = fx_add(ml, fx_mul_u32(fx_from_double(pi), sc[q]));
+    }
+  }
+  Fx Mtot;
+  uint32_t ctot;
+  Fx pre = block_exscan_fx(ml, sm.scan_f[1], Mtot);
+  uint32_t cpre = block_exscan_u32(cl, sm.scan_u2, ctot);
+  if (tid == 0) { sm.L = 0xffffffffu; sm.dMx = fx_zero(); }
+  tsync();
+  for (int j = 0; j < E; ++j) {
+    const int q = q0 + j;
+    if (q < (int)nd) {
+      const Fx mass = fx_mul_u32(fx_from_double(ev[q]), sc[q]);
+      const Fx incl = fx_add(pre, mass);
+      // outliers (key >= threshold) are a prefix of the sorted values: the last one holds their mass
+      if (pl.has_thr && sk[q] >= pl.key_thr && (q + 1 == (int)nd || sk[q + 1] < pl.key_thr)) sm.dMx = incl;
+      if (fx_ge(incl, pl.t_p) && !fx_ge(pre, pl.t_p)) {  // the (unique) crossing value
+        sm.L = (uint32_t)q; sm.dK = sk[q]; sm.dngt = cpre; sm.dneq = sc[q]; sm.dH = pre;
+      }
+      pre = incl;
+      cpre += sc[q];
+    }
+  }
+  tsync();
+  QRITA_TSTAMP(12);
+  res.ok = true;
+  res.mx = fx_to_double(sm.dMx);
+  res.hit = fx_ge(sm.dMx, pl.t_sp);
+  res.keep_all = !fx_ge(Mtot, pl.t_sp) || sm.L == 0xffffffffu;
+  if (!res.keep_all) {
+    res.K = sm.dK; res.n_gt = sm.dngt; res.n_eq = sm.dneq;
+    // smallest j with fsum(head + j * p_b) >= p (_min_dup_count, pivot_search.py:143-156), exactly
+    const double pb = ev[sm.L];
+    const Fx fb = fx_from_double(pb);
+    const Fx H = sm.dH;
+    const double jd = ceil(fx_to_double(fx_sub(pl.t_p, H)) / pb);
+    uint32_t j = (jd < 1.0) ? 1u : (jd > (double)res.n_eq ? res.n_eq : (uint32_t)jd);
+    while (j > 1u && fx_ge(fx_add(H, fx_mul_u32(fb, j - 1u)), pl.t_p)) --j;
+    while (j < res.n_eq && !fx_ge(fx_add(H, fx_mul_u32(fb, j)), pl.t_p)) ++j;
+    res.j = j;
+  }
+  tsync();
+  return res;
+}
+
+// select_nth_eq over a row in global memory with 16-byte vector loads (aligned rows): warp w owns a
+// contiguous run of vectors; per-lane W-bit match masks, warp sums, then one warp rescans its run.
+template <typename T>
+__device__ uint32_t select_nth_eq_row(const T *in, int V, uint32_t K, uint32_t c, TailSmem &sm) {
+  using VT = typename Vec<T>::type;
+  constexpr int W = Vec<T>::W;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const VT *pv = reinterpret_cast<const VT *>(in);
+  const int nv = V / W;
+  const int seg = ((nv + kWarps - 1) / kWarps + 31) & ~31;
+  const int beg = warp * seg, end = min(nv, beg + seg);
+  auto mask_of = [&](const VT &r) -> uint32_t {
+    uint32_t mk = 0u;
+#pragma unroll
+    for (int w = 0; w < W; ++w) mk |= (key_of_bits(lane_bits<T>(r, w)) == K ? 1u : 0u) << w;
+    return mk;
+  };
+  uint32_t cnt = 0u;
+  for (int base = beg; base < end; base += 32 * kLd) {
+    VT r[kLd];
+#pragma unroll
+    for (int j = 0; j < kLd; ++j) {
+      const int vi = base + 32 * j + lane;
+      if (vi < end) r[j] = __ldcg(pv + vi);
+    }
+#pragma unroll
+    for (int j = 0; j < kLd; ++j)
+      if (base + 32 * j + lane < end) cnt += (uint32_t)__popc(mask_of(r[j]));
+  }
+  cnt = warp_sum(cnt);
+  if (lane == 0) sm.sel[warp] = cnt;
+  tsync();
+  if (threadIdx.x == 0) {
+    uint32_t acc = 0u;
+    int w = 0;
+    for (; w < kWarps; ++w) {
+      if (acc + sm.sel[w] >= c) break;
+      acc += sm.sel[w];
+    }
+    sm.u[0] = (uint32_t)w;
+    sm.u[1] = c - acc;
+    sm.u[2] = kNoCut;
+  }
+  tsync();
+  if (warp == (int)sm.u[0]) {
+    uint32_t need = sm.u[1];
+    for (int base = beg; base < end; base += 32) {
+      const int vi = base + lane;
+      VT r;
+      uint32_t mk = 0u;
+      if (vi < end) { r = __ldcg(pv + vi); mk = mask_of(r); }
+      const uint32_t pc = (uint32_t)__popc(mk);
+      uint32_t incl = pc;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
+      }
+      const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
+      if (tot >= need) {
+        if (incl >= need && incl - pc < need) sm.u[2] = (uint32_t)(vi * W + nth_set_bit(mk, need - (incl - pc)));
+        break;
+      }
+      need -= tot;
+    }
+  }
+  tsync();
+  const uint32_t res = sm.u[2];
+  tsync();
+  return res;
+}
+
 __device__ __forceinline__ bool kept_by(uint32_t key, uint32_t idx, uint32_t K, uint32_t cut) {
   return key > K || (key == K && idx <= cut);
 }
@@ -1128,6 +1451,42 @@ __device__ __forceinline__ bool kept_by(uint32_t key, uint32_t idx, uint32_t K, 
 // 2 = -inf where not kept (in-place).
 template <typename T>
 __device__ void write_row(const T *in, T *out, int V, uint32_t K, uint32_t cut, int how) {
+  using VT = typename Vec<T>::type;
+  constexpr int W = Vec<T>::W;
+  if (((uintptr_t)in % 16) == 0 && ((uintptr_t)out % 16) == 0 && V % W == 0) {
+    const VT *pi = reinterpret_cast<const VT *>(in);
+    VT *po = reinterpret_cast<VT *>(out);
+    const int nv = V / W;
+    for (int v0 = threadIdx.x; v0 < nv; v0 += kThreads * kLd) {
+      VT r[kLd];
+#pragma unroll
+      for (int j = 0; j < kLd; ++j)
+        if (v0 + j * kThreads < nv) r[j] = __ldcg(pi + v0 + j * kThreads);
+#pragma unroll
+      for (int j = 0; j < kLd; ++j) {
+        const int vi = v0 + j * kThreads;
+        if (vi >= nv) continue;
+        VT o = r[j];
+        T *oe = reinterpret_cast<T *>(&o);
+        const T *ie = reinterpret_cast<const T *>(&r[j]);
+        bool any_kept = false, all_kept = true;
+#pragma unroll
+        for (int w = 0; w < W; ++w) {
+          const bool kp = kept_by(key_of_bits(Elem<T>::bits(ie[w])), (uint32_t)(vi * W + w), K, cut);
+          any_kept |= kp;
+          all_kept &= kp;
+          if (!kp) oe[w] = Elem<T>::neg_inf();
+        }
+        if (how == 1 || (how == 2 && !all_kept)) po[vi] = o;
+        else if (how == 0 && any_kept) {
+#pragma unroll
+          for (int w = 0; w < W; ++w)
+            if (kept_by(key_of_bits(Elem<T>::bits(ie[w])), (uint32_t)(vi * W + w), K, cut)) out[vi * W + w] = ie[w];
+        }
+      }
+    }
+    return;
+  }
   for (int i0 = threadIdx.x; i0 < V; i0 += kThreads * kLd) {
     T v[kLd];
 #pragma unroll
@@ -1147,15 +1506,6 @@ __device__ void write_row(const T *in, T *out, int V, uint32_t K, uint32_t cut, 
   }
 }
 
-// Debug phase timestamps of the row tail (QRITA_DEBUG_TIMING): P.dbg[row][i] = %globaltimer.
-__device__ __forceinline__ void tail_stamp(const Params &P, int row, int i) {
-  if ((P.flags & QRITA_DEBUG_TIMING) && threadIdx.x == 0) {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    P.dbg[(size_t)row * 16 + i] = t;
-  }
-}
-#define QRITA_TSTAMP(i) tail_stamp(P, row, (i))
 
 // Row tail proper, run by the tail thread group (kThreads threads, tsync barriers) once the row's
 // outliers X = (xb, xi)[0, n_c) are in shared memory (in any order; only when they fit: n_c <= kCapX
@@ -1169,7 +1519,8 @@ __device__ void tail_resolve(const Params &P, int row, const RowPlan &pl, uint32
                              uint8_t *work, TailSmem &sm, uint32_t n_c, bool overflow, uint32_t maxkey,
                              uint32_t minkey, uint32_t nf_col, uint32_t xcap, const uint32_t *gxb = nullptr,
                              const uint32_t *gxi = nullptr, uint32_t gcap = 0u,
-                             const uint32_t *hist_in = nullptr, int bsh_in = 0) {
+                             const uint32_t *hist_in = nullptr, int bsh_in = 0,
+                             size_t work_bytes = (size_t)kWorkBytes) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int V = P.V;
   const T *in = (const T *)P.logits + (size_t)row * P.ld_in;
@@ -1402,7 +1753,12 @@ __device__ void tail_resolve(const Params &P, int row, const RowPlan &pl, uint32
   QRITA_TSTAMP(3);
   const SrcX X{xb, xi, (int)n_c};
   const SrcRow<T> RW{in, V};
+  const bool row_vec = ((uintptr_t)in % 16) == 0 && V % Vec<T>::W == 0;
   Red red(sm);
+  // c-th copy of key K in index order (the duplicate-trimming rule of pipeline.py:53-56)
+  auto row_select = [&](uint32_t K, uint32_t c) -> uint32_t {
+    return row_vec ? select_nth_eq_row<T>(in, V, K, c, sm) : select_nth_eq(RW, K, c, red);
+  };
   red.act_key = (uint32_t *)ap;  // the top-k search runs first: the whole region holds keys
   red.act_pi = ap;
   red.act_cap_k = 3 * kCapA;
@@ -1431,13 +1787,40 @@ __device__ void tail_resolve(const Params &P, int row, const RowPlan &pl, uint32
     uint32_t ck = k - kr.n_gt;  // n_keep = n_dup - (N - k), pipeline.py:117
     if (nodup) ck = kr.n_eq;
     if (ck >= kr.n_eq) cutk = kNoCut;
-    else cutk = select_nth_eq(RW, Kk, ck, red);  // index order: scan the row itself
+    else cutk = row_select(Kk, ck);  // index order: scan the row itself
     n_s = kr.n_gt + ck;
     Kf = Kk; cutf = cutk; kept = n_s;
     QRITA_TSTAMP(4);
   }
 
   // ================= top-p stage: pipeline.py:161-196 (p only) and :226-239 (k then p) ============
+  // ================= top-p only over the whole row: distinct-value path =================
+  if (!sorted_out && mode == MODE_TOPP && NP == 3 && !nodup && (!x_fits || sizeof(T) == 2)) {
+    // table in X (2 x 4096 words); the kCapC probabilities behind the bin-sort layout when the work
+    // area has room (fused kernel: the 60 KB ring), else behind the table (staged: 64 KB X)
+    constexpr uint32_t cap = 4096u;
+    double *dev_pi = work_bytes >= (size_t)kWorkBytesBins + (size_t)kCapC * 8
+                         ? reinterpret_cast<double *>(work + kWorkBytesBins)
+                         : reinterpret_cast<double *>(xb + 2 * cap);
+    const DistinctRes dr = distinct_topp<T>(P, row, in, V, m, pl, xb, xb + cap, cap, cb, ci, db, di, hc, he, dev_pi, sm);
+    if (dr.ok) {
+      met.outlier_prob_sum = sigma ? dr.mx : 0.0;
+      met.trunc_hit = (sigma && dr.hit && !force_fb) ? 1 : 0;
+      met.fallback_used = met.trunc_hit ? 0 : 1;
+      met.p_search_iters = 1;
+      full_row = true;
+      sorted_out = true;  // the stages below are done
+      if (dr.keep_all) { Kf = 0u; cutf = kNoCut; kept = (uint32_t)V; }
+      else {
+        Kf = dr.K;
+        kept = dr.n_gt + dr.j;
+        cutf = dr.j >= dr.n_eq ? kNoCut : row_select(dr.K, dr.j);
+      }
+      QRITA_TSTAMP(13);
+    }
+  }
+  const bool distinct_done = sorted_out && mode == MODE_TOPP;
+
   if (!sorted_out && (mode == MODE_TOPP || mode == MODE_TOPKP)) {
     red.act_key = ak;  // (key, probability) pairs from here on
     const Fx Tp = pl.t_p, Tsp = pl.t_sp;
@@ -1555,7 +1938,7 @@ __device__ void tail_resolve(const Params &P, int row, const RowPlan &pl, uint32
         // whole cluster (within S); if it is the top-k boundary cluster the top-k cut still applies
         cutf = (!topp_only && pr.K == Kk) ? cutk : kNoCut;
       } else {
-        cutf = select_nth_eq(RW, pr.K, j, red);  // index order: scan the row itself
+        cutf = row_select(pr.K, j);  // index order: scan the row itself
       }
     }
   }
@@ -1566,7 +1949,7 @@ __device__ void tail_resolve(const Params &P, int row, const RowPlan &pl, uint32
     write_row<T>(in, out, V, Kf, cutf, inplace ? 2 : 1);  // the stream left top-p-only rows alone
   } else if (inplace) {
     write_row<T>(in, out, V, Kf, cutf, 2);
-  } else if (sorted_out) {
+  } else if (sorted_out && !distinct_done) {
     for (int q = tid; q < (int)kept; q += kThreads) out[di[q]] = Elem<T>::from_bits(db[q]);
   } else if (k_used_x) {
     for (int i = tid; i < X.n; i += kThreads) {
@@ -1653,32 +2036,6 @@ __global__ void __launch_bounds__(kThreads, 2) qrita_tail(Params P) {
 // ------------------------------------------------------------------------------------------------
 // K1: streaming pass + row tails
 // ------------------------------------------------------------------------------------------------
-template <typename T> struct Vec;
-template <> struct Vec<float> { using type = float4; static constexpr int W = 4; };
-template <> struct Vec<uint16_t> { using type = uint4; static constexpr int W = 8; };
-
-template <typename T>
-__device__ __forceinline__ uint32_t lane_bits(const typename Vec<T>::type &v, int w);
-template <>
-__device__ __forceinline__ uint32_t lane_bits<float>(const float4 &v, int w) {
-  return __float_as_uint(w == 0 ? v.x : w == 1 ? v.y : w == 2 ? v.z : v.w);
-}
-template <>
-__device__ __forceinline__ uint32_t lane_bits<uint16_t>(const uint4 &v, int w) {
-  const uint32_t x = (w >> 1) == 0 ? v.x : (w >> 1) == 1 ? v.y : (w >> 1) == 2 ? v.z : v.w;
-  return (w & 1) ? (x & 0xffff0000u) : (x << 16);
-}
-
-template <typename T>
-__device__ __forceinline__ typename Vec<T>::type neg_inf_vec();
-template <> __device__ __forceinline__ float4 neg_inf_vec<float>() {
-  const float n = __uint_as_float(0xff800000u);
-  return make_float4(n, n, n, n);
-}
-template <> __device__ __forceinline__ uint4 neg_inf_vec<uint16_t>() {
-  return make_uint4(0xff80ff80u, 0xff80ff80u, 0xff80ff80u, 0xff80ff80u);
-}
-
 // One warp streams one 1024-element chunk: 128-bit loads (8 per lane for fp32, 4 for bf16), chunk
 // max / min / first non-finite column, order-stable outlier compaction with ballot/popc straight
 // into the chunk's HBM slots, and the output background (-inf for top-k rows, a copy for
@@ -1922,7 +2279,8 @@ template <typename T>
 __device__ __forceinline__ void consume_chunk(const uint8_t *stage, int c0, int n, float thr, bool write_bg,
                                               bool write_copy, T *dst, uint32_t *n_x, uint32_t *xb,
                                               uint32_t *xi, uint32_t *gxb, uint32_t *gxi, uint32_t gcap,
-                                              uint32_t *hist, uint32_t bl, int bsh, float &rmx, float &ramx) {
+                                              uint32_t *hist, uint32_t bl, int bsh, bool do_hist, float &rmx,
+                                              float &ramx) {
   using VT = typename Vec<T>::type;
   constexpr int W = Vec<T>::W;
   constexpr int CE = kStageBytes / (int)sizeof(T);
@@ -1978,6 +2336,10 @@ __device__ __forceinline__ void consume_chunk(const uint8_t *stage, int c0, int 
   }
   const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
   if (total == 0u) return;
+  if (*(volatile uint32_t *)n_x >= (uint32_t)kCapXF + gcap) {  // X is full: only count (metrics)
+    if (lane == 31) atomicAdd(n_x, total);
+    return;
+  }
   uint32_t base = 0u;
   if (lane == 31) base = atomicAdd(n_x, total);
   uint32_t pos = __shfl_sync(0xffffffffu, base, 31) + incl - cnt;
@@ -1986,8 +2348,10 @@ __device__ __forceinline__ void consume_chunk(const uint8_t *stage, int c0, int 
     m &= m - 1;
     const int e = ((j / W) * 32 + lane) * W + (j % W);
     const uint32_t bits = Elem<T>::bits(st[e]);
-    const uint32_t bin = (key_of_bits(bits) - bl - 1u) >> bsh;
-    atomicAdd(&hist[bin < (uint32_t)kNB ? bin : (uint32_t)(kNB - 1)], 1u);
+    if (do_hist) {
+      const uint32_t bin = (key_of_bits(bits) - bl - 1u) >> bsh;
+      atomicAdd(&hist[bin < (uint32_t)kNB ? bin : (uint32_t)(kNB - 1)], 1u);
+    }
     if (pos < (uint32_t)kCapXF) {
       xb[pos] = bits; xi[pos] = (uint32_t)(c0 + e);
     } else if (pos - (uint32_t)kCapXF < gcap) {  // spill past shared memory into the row's HBM buffer
@@ -2065,7 +2429,7 @@ __global__ void __launch_bounds__(kFusedThreads, 2) qrita_fused(Params P) {
         stage_wait(fs, g);
         consume_chunk<T>(ring + (size_t)slot * kStageBytes, c * CE, min(CE, V - c * CE), thr, write_bg,
                          write_copy, dst + (size_t)c * CE, &fs.n_x, xb, xi, gxb, gxi, (uint32_t)P.xcap, fs.hist,
-                         pl.key_thr - 1u, pl.bsh, rmx, ramx);
+                         pl.key_thr - 1u, pl.bsh, mode == MODE_TOPK || mode == MODE_TOPKP, rmx, ramx);
         __syncwarp();
         if (lane == 0) mbar_arrive(&fs.empty[slot]);
       }
@@ -2086,7 +2450,8 @@ __global__ void __launch_bounds__(kFusedThreads, 2) qrita_fused(Params P) {
       }
       // (3) resolve; every stage of this row has been consumed, so the ring is the work area
       tail_resolve<T, NP>(P, row, pl, xb, xi, ring, fs.tail, fs.n_x, false, maxkey, minkey, nf_col,
-                          (uint32_t)kCapXF, gxb, gxi, (uint32_t)P.xcap, fs.hist, pl.bsh);
+                          (uint32_t)kCapXF, gxb, gxi, (uint32_t)P.xcap, fs.hist, pl.bsh,
+                          (size_t)kRing * kStageBytes);
     }
     g0 += (uint32_t)nch;
     __syncthreads();  // row done: the ring and X may be refilled

@@ -167,8 +167,10 @@ if len(sys.argv) > 1 and sys.argv[1] == "ftiming":
             d = (a[ok, j] - a[ok, i]) / 1e3
             if ok.any():
                 print(f"   {nm:8s} mean {d.mean():7.2f} us  min {d.min():7.2f}  max {d.max():7.2f}")
-        for nm, i, j in (("binscan", 2, 10), ("scatter", 10, 11), ("fixup+e", 11, 12), ("D", 12, 13),
-                         ("piscan", 13, 14), ("cross", 14, 3), ("output", 3, 9)):
+        sub = ((("binscan", 2, 10), ("scatter", 10, 11), ("fixup+e", 11, 12), ("D", 12, 13),
+                ("piscan", 13, 14), ("cross", 14, 3), ("output", 3, 9)) if cfg != "cfg3" else
+               (("count", 2, 10), ("sort", 10, 11), ("masses", 11, 12), ("select", 12, 13), ("output", 13, 9)))
+        for nm, i, j in sub:
             ok = (a[:, i] > 0) & (a[:, j] > 0)
             d = (a[ok, j] - a[ok, i]) / 1e3
             if ok.any():
