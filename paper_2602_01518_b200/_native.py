@@ -10,7 +10,7 @@ import ctypes
 import os
 
 LIB_DIR = os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib")
-LIB_PATH = os.path.join(LIB_DIR, "libqrita_b200.so")
+LIB_PATH = os.environ.get("QRITA_LIB") or os.path.join(LIB_DIR, "libqrita_b200.so")  # QRITA_LIB: A/B builds
 
 # include/qrita_b200.h enums
 DTYPE_F32 = 0

@@ -125,32 +125,22 @@ __device__ __forceinline__ Fx fx_mul_u32(const Fx &a, uint32_t j) {
   return r;
 }
 
-// Correctly rounded (nearest-even) conversion to double.
+// Correctly rounded (nearest-even) conversion to double.  No dynamically indexed arrays (those
+// would live in local memory): the top non-zero word is selected explicitly.
 __device__ __forceinline__ double fx_to_double(const Fx &a) {
-  unsigned long long w[3] = {a.w0, a.w1, a.w2};
-  int top = 2;
-  while (top >= 0 && w[top] == 0ull) --top;
-  if (top < 0) return 0.0;
-  int lz = __clzll((long long)w[top]);
-  int P = top * 64 + (63 - lz);  // index of the highest set bit
-  if (P < 64) {
-    return ldexp((double)w[0], -128);  // exact integer < 2^64, cvt.rn rounds correctly
+  unsigned long long hi, mid, lo;
+  int base;  // bit index of hi's least significant bit in the 192-bit integer
+  if (a.w2) { hi = a.w2; mid = a.w1; lo = a.w0; base = 128; }
+  else if (a.w1) { hi = a.w1; mid = a.w0; lo = 0ull; base = 64; }
+  else {
+    // an integer < 2^64: cvt.rn rounds correctly, the power-of-two scale is exact
+    return a.w0 ? ldexp(__ull2double_rn(a.w0), -128) : 0.0;
   }
-  // 64-bit window [P-63, P] plus sticky
-  int lowbit = P - 63;
-  int limb = lowbit >> 6, off = lowbit & 63;
-  unsigned long long win, sticky;
-  if (off == 0) {
-    win = w[limb];
-    sticky = 0ull;
-    for (int i = 0; i < limb; ++i) sticky |= w[i];
-  } else {
-    win = (w[limb] >> off) | (w[limb + 1] << (64 - off));
-    sticky = w[limb] & ((1ull << off) - 1ull);
-    for (int i = 0; i < limb; ++i) sticky |= w[i];
-  }
-  if (sticky) win |= 1ull;  // below the rounding position of a 64->53 bit conversion
-  return ldexp(__ull2double_rn(win), lowbit - 128);
+  const int lz = __clzll((long long)hi);
+  // 64-bit window starting at the top set bit, plus a sticky bit for everything below it
+  const unsigned long long win = lz ? (hi << lz) | (mid >> (64 - lz)) : hi;
+  const unsigned long long rest = (lz ? (mid << lz) : mid) | lo;
+  return ldexp(__ull2double_rn(rest ? (win | 1ull) : win), base - lz - 128);
 }
 
 // Smallest fixed-point value S with round_to_nearest_even(S) >= p, for a double 0 < p <= 1.

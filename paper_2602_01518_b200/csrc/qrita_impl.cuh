@@ -1,4 +1,4 @@
-// qrita_kernels.cu — B200 (sm_100a) exact Top-k / Top-p truncation and its C ABI.
+// qrita_impl.cuh — B200 (sm_100a) exact Top-k / Top-p truncation kernels.
 //
 // Reference path (arxiv/paper_2602_01518, pkg/src/sigmatop):
 //   engine.run_batch (engine.py:82-113) -> pipeline.truncate_topk_topp (pipeline.py:199-239)
@@ -8,20 +8,17 @@
 //     -> pipeline.finalize_mask / _apply_plan (pipeline.py:47-78)
 // Ground truth: oracle.oracle_topk_topp (oracle.py:70-89).
 //
-// B200 design (DESIGN.md has the full story):
-//   K0 qrita_prep     one CTA per row: sigma statistics over the sample prefix (bit-replica of
-//                     numpy's pairwise mean, so thresholds equal the reference's), table lookup,
-//                     threshold key, exact fixed-point nucleus thresholds for p.
-//   K1 qrita_main     persistent, dynamically scheduled over (row, chunk) work items.  Each item
-//                     streams a 16K-element chunk once from HBM with 128-bit loads, reduces the
-//                     chunk max / non-finite flag, compacts the sigma outliers in index order into a
-//                     small per-chunk HBM scratch (warp ballot/popc + block scan) and writes the -inf
-//                     background of the output.  The CTA that completes a row's last chunk runs the
-//                     row tail: quaternary key-space pivot search over the outliers staged in shared
-//                     memory (top-k), fp64 softmax over the survivors with an exact 192-bit
-//                     fixed-point normaliser and nucleus masses (top-p), duplicate trimming by index
-//                     order, and the scatter of the kept logits.  Rows that miss the pre-filter are
-//                     searched over the full row instead.  1 HBM read + 1 HBM write per element.
+// Two pipelines behind one C entry point (DESIGN.md has the full story):
+//   qrita_fused  (default; rows 16-byte aligned) one launch, one CTA owns one row at a time, two
+//                CTAs per SM, persistent over rows.  The row streams once through a ring of 4 KB
+//                shared-memory stages filled by bulk copies (cp.async.bulk + mbarrier); the sigma plan
+//                is computed in place from the first stages; outliers are compacted straight into
+//                shared memory while the -inf / copy background is written; the row tail (bin-sort
+//                resolve, or the pivot searches / distinct-value path on the rare full-row cases)
+//                runs in the same CTA on the same shared memory.
+//   staged       (unaligned rows, or QRITA_STAGED) qrita_prep -> qrita_stream -> qrita_tail chained
+//                with programmatic dependent launch; outliers go through per-row HBM buffers.
+// Both share tail_resolve and compute bit-identical results.
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -194,6 +191,13 @@ __device__ double pairwise_tree(int n, LeafFn leaf) {
   }
 }
 
+// Serial replay of the pairwise sums straight from global memory (non-default sample sizes only);
+// out of line, so its explicit stack stays out of the hot kernels' frames.
+template <typename T, bool SQUARE>
+__device__ __noinline__ double pairwise_serial(const T *a, int n) {
+  return pairwise_tree(n, [&](int o, int m) -> double { return leaf_sum<T, SQUARE>(a + o, m); });
+}
+
 // Smallest s with w <= kNB * 2^s: key bins (l, l + 2^s], (l + 2^s, l + 2^(s+1)], ... cover (l, l + w].
 __device__ __forceinline__ int bin_shift(uint32_t w) {
   if (w <= (uint32_t)kNB) return 0;
@@ -355,8 +359,7 @@ __device__ void plan_sample(const Params &P, SampleAt xs, const T *a, PlanScratc
     if (tid < 2) sc.res[tid] = sc.val[tid][nl + tr.n_internal - 1 < nl ? 0 : nl + tr.n_internal - 1];
   } else if (tid < 2) {  // long samples (non-default sample_size): serial replay from global
     sc.res[tid] = tid == 0
-        ? pairwise_tree(n, [&](int o, int m) -> double { return leaf_sum<T, false>(a + o, m); })
-        : pairwise_tree(n, [&](int o, int m) -> double { return leaf_sum<T, true>(a + o, m); });
+        ? pairwise_serial<T, false>(a, n) : pairwise_serial<T, true>(a, n);
   }
   tsync();
 finish:
@@ -920,13 +923,20 @@ __device__ KRes search_k(const Src &src, uint32_t l, uint32_t r, uint32_t cl, ui
       int J = -1;  // largest pivot still holding >= k keys above it
 #pragma unroll
       for (int j = 0; j < NP; ++j) J = (cnt[j] >= k) ? j : J;
+      // pick the J and J+1 entries with unrolled selects (no dynamically indexed local arrays)
+      uint32_t cJ = 0u, mJ = 0u, xJ = 0u, pJ = 0u, cJ1 = 0u, pJ1 = 0u;
+#pragma unroll
+      for (int j = 0; j < NP; ++j) {
+        if (j == J) { cJ = cnt[j]; mJ = mn[j]; xJ = mc[j]; pJ = piv[j]; }
+        if (j == J + 1) { cJ1 = cnt[j]; pJ1 = piv[j]; }
+      }
       if (threadIdx.x == 0) {
         st.iters += 1;
-        if (J >= 0 && cnt[J] - mc[J] < k) {
-          st.done = 1u; st.K = mn[J]; st.n_gt = cnt[J] - mc[J]; st.n_eq = mc[J];
+        if (J >= 0 && cJ - xJ < k) {
+          st.done = 1u; st.K = mJ; st.n_gt = cJ - xJ; st.n_eq = xJ;
         } else {
-          if (J >= 0) { st.l = piv[J]; st.cl = cnt[J]; }
-          if (J + 1 < NP) { st.r = piv[J + 1]; st.cr = cnt[J + 1]; }
+          if (J >= 0) { st.l = pJ; st.cl = cJ; }
+          if (J + 1 < NP) { st.r = pJ1; st.cr = cJ1; }
           const uint32_t n_in = st.cl - st.cr;
           if (!act && (int)n_in <= R.act_cap_k && 2 * (int)n_in <= n) st.compact = 1;
         }
@@ -1216,7 +1226,7 @@ struct DistinctRes {
 // of a pivot search with an fp64 exp per element per pass.  tk/tc: table of cap (power of two)
 // entries; lk/lc, sk/sc: kCapC-entry lists; hc/he: kNB bins; ev: kCapC doubles.
 template <typename T>
-__device__ DistinctRes distinct_topp(const Params &P, int row, const T *in, int V, double m, const RowPlan &pl, uint32_t *tk,
+__device__ __noinline__ DistinctRes distinct_topp(const Params &P, int row, const T *in, int V, double m, const RowPlan &pl, uint32_t *tk,
                                      uint32_t *tc, uint32_t cap, uint32_t *lk, uint32_t *lc, uint32_t *sk,
                                      uint32_t *sc, uint32_t *hc, uint32_t *he, double *ev, TailSmem &sm) {
   // lk/lc: compacted table, then the sorted result; sk/sc: grouped by bin
@@ -1382,7 +1392,7 @@ __device__ uint32_t select_nth_eq_row(const T *in, int V, uint32_t K, uint32_t c
   const int nv = V / W;
   const int seg = ((nv + kWarps - 1) / kWarps + 31) & ~31;
   const int beg = warp * seg, end = min(nv, beg + seg);
-  auto mask_of = [&](const VT &r) -> uint32_t {
+  auto mask_of = [&](VT r) -> uint32_t {
     uint32_t mk = 0u;
 #pragma unroll
     for (int w = 0; w < W; ++w) mk |= (key_of_bits(lane_bits<T>(r, w)) == K ? 1u : 0u) << w;
@@ -1390,15 +1400,11 @@ __device__ uint32_t select_nth_eq_row(const T *in, int V, uint32_t K, uint32_t c
   };
   uint32_t cnt = 0u;
   for (int base = beg; base < end; base += 32 * kLd) {
-    VT r[kLd];
 #pragma unroll
     for (int j = 0; j < kLd; ++j) {
       const int vi = base + 32 * j + lane;
-      if (vi < end) r[j] = __ldcg(pv + vi);
+      if (vi < end) cnt += (uint32_t)__popc(mask_of(__ldcg(pv + vi)));
     }
-#pragma unroll
-    for (int j = 0; j < kLd; ++j)
-      if (base + 32 * j + lane < end) cnt += (uint32_t)__popc(mask_of(r[j]));
   }
   cnt = warp_sum(cnt);
   if (lane == 0) sm.sel[warp] = cnt;
@@ -2198,10 +2204,6 @@ __global__ void __launch_bounds__(kStreamThreads, 3) qrita_stream(Params P) {
       st_keep_u32(P.cand_idx + rb + pos + j, s_ci[wib][j], keep_pol);
     }
     __syncwarp();
-    if (P.exp_publish && lane == 0) {  // EXPERIMENT: per-chunk release of the row counter
-      __threadfence();
-      atomicAdd(&ag->done, 1u);
-    }
   }
   if (!waited) pdl_wait();
 }
@@ -2209,18 +2211,21 @@ __global__ void __launch_bounds__(kStreamThreads, 3) qrita_stream(Params P) {
 // ------------------------------------------------------------------------------------------------
 // Fused single-kernel pipeline: one CTA owns one row at a time
 // ------------------------------------------------------------------------------------------------
-// CTA = kThreads tail/consumer threads (8 warps) + 1 TMA producer warp; two CTAs per SM, persistent
-// over rows (row = blockIdx.x + i * gridDim.x).  Per row:
-//   producer  streams the row through a ring of kRing 4 KB shared-memory stages with bulk copies
-//             (cp.async.bulk, L2 evict_first) completing on per-stage mbarriers;
-//   consumers (1) compute the sigma plan from the first sample stages in place (compute_plan: the
-//             numpy pairwise statistics of sigma_trunc.py:69-103), (2) consume the chunks warp by
-//             warp: NaN-propagating row extrema, outliers (z >= threshold) appended straight into
-//             shared memory X with warp-aggregated slots, the -inf (or copy) background written to
-//             HBM with streaming 128-bit stores, (3) run tail_resolve on X with the ring reused as
-//             its work area.
-// The row never leaves the SM between reading and resolving: no outlier workspace, no inter-kernel
-// dependency, one launch per call.  The other CTA on the SM streams while this one resolves.
+// CTA = 8 warps (kThreads), two CTAs per SM (128 registers each), persistent over rows
+// (row = blockIdx.x + i * gridDim.x).  Per row:
+//   ring      the row streams through kRing 4 KB shared-memory stages filled by bulk copies
+//             (cp.async.bulk, L2 evict_first) that complete on per-stage mbarriers; thread 0 fills the
+//             ring at row start, then the warp that consumes chunk c refills its stage with chunk
+//             c + kRing (no producer warp, no empty barriers);
+//   plan      the sigma plan is computed from the first sample stages in place (plan_begin /
+//             plan_sample: the numpy pairwise statistics of sigma_trunc.py:69-103);
+//   stream    warp w consumes chunks w, w + 8, ...: row max and NaN-propagating max |x|, outliers
+//             (z >= threshold) appended straight into shared memory X with one warp-aggregated slot
+//             reservation per chunk and counted into key bins, the -inf (or copy) background written
+//             to HBM with streaming 128-bit stores;
+//   resolve   tail_resolve on X, with the ring reused as its work area.
+// The row never leaves the SM between reading and resolving: no inter-kernel dependency, one launch
+// per call; the other CTA on the SM streams while this one resolves.
 // Shared memory per CTA (two CTAs per SM, <= 113 KB each): X = kCapXF outliers (44 KB; further ones
 // spill to the row's HBM buffer) + a ring of kRing 4 KB stages (60 KB in flight per CTA, 120 KB per
 // SM), which doubles as the tail's work area once the row is consumed, + the outliers' key-bin
@@ -2228,7 +2233,7 @@ __global__ void __launch_bounds__(kStreamThreads, 3) qrita_stream(Params P) {
 constexpr int kStageBytes = 4096;
 constexpr int kCapXF = 5632;
 constexpr int kRing = 15;
-constexpr int kFusedThreads = kThreads + 32;
+constexpr int kFusedThreads = kThreads;  // 8 warps: stream, plan and resolve (no producer warp)
 static_assert(kRing >= 8, "ring must hold the sigma sample (<= 6 stages) plus slack");
 static_assert(kRing * kStageBytes >= kWorkBytes, "the ring doubles as the tail work area");
 static_assert(sizeof(PlanScratch) <= (size_t)kCapXF * 8, "plan scratch aliases the outlier area");
@@ -2237,7 +2242,6 @@ struct FusedSmem {
   TailSmem tail;
   RowPlan pl;
   unsigned long long full[kRing];   // stage filled (TMA transaction bytes)
-  unsigned long long empty[kRing];  // stage consumed (one consumer warp)
   uint32_t seq[kRing];              // chunk sequence number last issued into the stage
   uint32_t n_x;                     // outliers of the current row (all of them, even past kCapX)
   uint32_t hist[kNB];               // outliers per key bin (tail_resolve's bin sort)
@@ -2275,12 +2279,11 @@ template <> struct MaskT<64> { using type = unsigned long long; };
 // element: a 3-input max (row max), a 3-input NaN-propagating max of |x| (non-finite detection), one
 // compare folded into a per-lane outlier bit mask.  Then one warp scan + one shared atomic reserve
 // the chunk's slots in X, and each lane copies its outliers (re-read from the stage by bit index).
-template <typename T>
+template <typename T, bool HIST>
 __device__ __forceinline__ void consume_chunk(const uint8_t *stage, int c0, int n, float thr, bool write_bg,
                                               bool write_copy, T *dst, uint32_t *n_x, uint32_t *xb,
                                               uint32_t *xi, uint32_t *gxb, uint32_t *gxi, uint32_t gcap,
-                                              uint32_t *hist, uint32_t bl, int bsh, bool do_hist, float &rmx,
-                                              float &ramx) {
+                                              uint32_t *hist, uint32_t bl, int bsh, float &rmx, float &ramx) {
   using VT = typename Vec<T>::type;
   constexpr int W = Vec<T>::W;
   constexpr int CE = kStageBytes / (int)sizeof(T);
@@ -2336,19 +2339,17 @@ __device__ __forceinline__ void consume_chunk(const uint8_t *stage, int c0, int 
   }
   const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
   if (total == 0u) return;
-  if (*(volatile uint32_t *)n_x >= (uint32_t)kCapXF + gcap) {  // X is full: only count (metrics)
-    if (lane == 31) atomicAdd(n_x, total);
-    return;
-  }
   uint32_t base = 0u;
   if (lane == 31) base = atomicAdd(n_x, total);
-  uint32_t pos = __shfl_sync(0xffffffffu, base, 31) + incl - cnt;
+  base = __shfl_sync(0xffffffffu, base, 31);
+  if (base >= (uint32_t)kCapXF + gcap) return;  // X is full: the outliers are only counted
+  uint32_t pos = base + incl - cnt;
   while (m) {
     const int j = __ffsll((long long)m) - 1;
     m &= m - 1;
     const int e = ((j / W) * 32 + lane) * W + (j % W);
     const uint32_t bits = Elem<T>::bits(st[e]);
-    if (do_hist) {
+    if (HIST) {
       const uint32_t bin = (key_of_bits(bits) - bl - 1u) >> bsh;
       atomicAdd(&hist[bin < (uint32_t)kNB ? bin : (uint32_t)(kNB - 1)], 1u);
     }
@@ -2375,35 +2376,31 @@ __global__ void __launch_bounds__(kFusedThreads, 2) qrita_fused(Params P) {
   if (tid == 0) {
     for (int i = 0; i < kRing; ++i) {
       mbar_init(&fs.full[i], 1u);
-      mbar_init(&fs.empty[i], 1u);
       fs.seq[i] = 0xffffffffu;
     }
     mbar_fence_init();
   }
   __syncthreads();
-  uint32_t g0 = 0u;  // chunks of this CTA's earlier rows: stage sequence shared by producer and consumers
+  const unsigned long long pol = l2_evict_first_policy();
+  uint32_t g0 = 0u;  // chunks of this CTA's earlier rows: the ring's stage sequence
   for (int row = blockIdx.x; row < P.B; row += gridDim.x) {
     const T *in = (const T *)P.logits + (size_t)row * P.ld_in;
-    if (warp == kWarps) {
-      // ---------------- producer: the whole row through the ring ----------------
-      if (lane == 0) {
-        const unsigned long long pol = l2_evict_first_policy();
-        fence_proxy_async_smem();  // the previous row's tail wrote the ring through the generic proxy
-        for (int c = 0; c < nch; ++c) {
-          const uint32_t g = g0 + (uint32_t)c, slot = g % kRing;
-          mbar_wait(&fs.empty[slot], ((g / kRing) & 1u) ^ 1u);
-          *(volatile uint32_t *)&fs.seq[slot] = g;  // before the copy: consumers may wait on its parity
-          const uint32_t bytes = (uint32_t)(min(CE, V - c * CE) * (int)sizeof(T));
-          mbar_arrive_expect_tx(&fs.full[slot], bytes);
-          tma_load_1d(ring + (size_t)slot * kStageBytes, in + (size_t)c * CE, bytes, &fs.full[slot], pol);
-        }
-      }
-      __syncwarp();
-    } else {
-      // ---------------- consumers ----------------
+    // chunk c of the row -> stage (g0 + c) % kRing; seq records the chunk before its copy is issued
+    auto issue = [&](int c) {
+      const uint32_t g = g0 + (uint32_t)c, slot = g % kRing;
+      *(volatile uint32_t *)&fs.seq[slot] = g;
+      const uint32_t bytes = (uint32_t)(min(CE, V - c * CE) * (int)sizeof(T));
+      mbar_arrive_expect_tx(&fs.full[slot], bytes);
+      tma_load_1d(ring + (size_t)slot * kStageBytes, in + (size_t)c * CE, bytes, &fs.full[slot], pol);
+    };
+    if (tid == 0) {  // fill the ring; afterwards each consumed stage is refilled by its consumer
+      fence_proxy_async_smem();  // the previous row's tail wrote the ring through the generic proxy
+      for (int c = 0; c < kRing && c < nch; ++c) issue(c);
+    }
+    {
       QRITA_TSTAMP(0);
       // (1) plan: the sample-independent part while the first stages land, then the sample in place
-      if (tid == 0) { fs.n_x = 0u; plan_begin(P, row, &fs.pl); }
+      if (tid == 32) { fs.n_x = 0u; plan_begin(P, row, &fs.pl); }  // warp 1, while warp 0 fills the ring
       const int ns = P.tree.n_leaves > 0 ? (P.tree.n + CE - 1) / CE : 0;
       for (int i = tid; i < kNB; i += kThreads) fs.hist[i] = 0u;
       for (int j = 0; j < ns; ++j) stage_wait(fs, g0 + (uint32_t)j);
@@ -2414,10 +2411,13 @@ __global__ void __launch_bounds__(kFusedThreads, 2) qrita_fused(Params P) {
       }, in, *reinterpret_cast<PlanScratch *>(dsmem), &fs.pl);
       tsync();
       QRITA_TSTAMP(1);
-      const RowPlan pl = fs.pl;
+      const RowPlan &pl = fs.pl;  // read from shared memory on use (keeps the stream loop's registers free)
       const bool inplace = (P.flags & QRITA_INPLACE) != 0;
       const int mode = pl.mode;
       const float thr = pl.has_thr ? __uint_as_float(bits_of_key(pl.key_thr)) : __uint_as_float(0x7fffffffu);
+      const bool hist = mode == MODE_TOPK || mode == MODE_TOPKP;
+      const uint32_t bl = pl.key_thr - 1u;
+      const int bsh = pl.bsh;
       const bool write_bg = !inplace && (mode == MODE_TOPK || mode == MODE_TOPKP || mode == MODE_INVALID);
       const bool write_copy = !inplace && mode == MODE_PASS;
       T *dst = (T *)P.out + (size_t)row * P.ld_out;
@@ -2427,11 +2427,19 @@ __global__ void __launch_bounds__(kFusedThreads, 2) qrita_fused(Params P) {
       for (int c = warp; c < nch; c += kWarps) {
         const uint32_t g = g0 + (uint32_t)c, slot = g % kRing;
         stage_wait(fs, g);
-        consume_chunk<T>(ring + (size_t)slot * kStageBytes, c * CE, min(CE, V - c * CE), thr, write_bg,
-                         write_copy, dst + (size_t)c * CE, &fs.n_x, xb, xi, gxb, gxi, (uint32_t)P.xcap, fs.hist,
-                         pl.key_thr - 1u, pl.bsh, mode == MODE_TOPK || mode == MODE_TOPKP, rmx, ramx);
+        if (hist)
+          consume_chunk<T, true>(ring + (size_t)slot * kStageBytes, c * CE, min(CE, V - c * CE), thr, write_bg,
+                                 write_copy, dst + (size_t)c * CE, &fs.n_x, xb, xi, gxb, gxi, (uint32_t)P.xcap,
+                                 fs.hist, bl, bsh, rmx, ramx);
+        else
+          consume_chunk<T, false>(ring + (size_t)slot * kStageBytes, c * CE, min(CE, V - c * CE), thr, write_bg,
+                                  write_copy, dst + (size_t)c * CE, &fs.n_x, xb, xi, gxb, gxi, (uint32_t)P.xcap,
+                                  fs.hist, bl, bsh, rmx, ramx);
         __syncwarp();
-        if (lane == 0) mbar_arrive(&fs.empty[slot]);
+        if (lane == 0 && c + kRing < nch) {  // refill this stage with the chunk kRing ahead
+          fence_proxy_async_smem();
+          issue(c + kRing);
+        }
       }
       {
         const uint32_t mx = warp_max(key_of_bits(__float_as_uint(rmx)));
@@ -2500,9 +2508,7 @@ static cudaError_t launch_pipeline(const Params &P, cudaStream_t st, cudaEvent_t
     if (want < 1) want = 1;
     stream_grid = sms * (per_sm < want ? (per_sm < 1 ? 1 : per_sm) : want);
   }
-  Params Pm = P;
-  Pm.exp_publish = getenv("QRITA_EXP_PUBLISH") ? atoi(getenv("QRITA_EXP_PUBLISH")) : 0;
-  const Params &PP = Pm;
+  const Params &PP = P;
   qrita_prep<T><<<P.B, 256, 0, st>>>(PP);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;

@@ -105,7 +105,6 @@ struct Params {
   unsigned long long *dbg;  // [B][16] phase timestamps of the row tail (QRITA_DEBUG_TIMING)
   int nchunks;
   int total_items;
-  int exp_publish;
   int xcap;                 // row_cap(V)
   PwTree tree;
 };
