@@ -1,0 +1,10 @@
+# Round evidence (run under gpurun): ncu launch lists for every config and one --set full capture of
+# the dominant kernel (qrita_fused, cfg2).  Numbers printed under ncu are never bench values.
+mkdir -p gpurun_out/prof
+for c in cfg2 cfg4 cfg3 cfg1 cfg2copy; do
+  ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
+      -k regex:qrita -s 3 -c 3 --csv --log-file gpurun_out/prof/launches_$c.csv \
+      python bench.py --config $c --steps 3 --warmup 3 --no-extras > /dev/null 2>&1
+done
+ncu --set full --clock-control none --import-source on -k regex:qrita_fused -s 3 -c 1 \
+    -o gpurun_out/prof/fused_cfg2 python bench.py --steps 1 --warmup 3 --no-extras > gpurun_out/prof/fused_cfg2.log 2>&1
