@@ -1240,15 +1240,15 @@ __device__ __noinline__ DistinctRes distinct_topp(const Params &P, int row, cons
   tsync();
   // 1. count every distinct key (keys of finite logits are >= 1; 0 marks an empty slot)
   for_row_warp<T>(in, V, [&](int, bool valid, uint32_t bits) {
-    const uint32_t key = valid ? key_of_bits(bits) : 0u;
-    const uint32_t peers = __match_any_sync(0xffffffffu, key);
-    if (!valid || lane != __ffs((int)peers) - 1 || sm.dabort) return;
-    const uint32_t n = (uint32_t)__popc(peers);
+    if (!valid) return;
+    const uint32_t key = key_of_bits(bits);
+    const uint32_t n = 1u;  // per-lane atomics: cheaper than match_any aggregation here
     uint32_t h = (key * 0x9E3779B1u) >> (32u - lg);
     for (uint32_t probe = 0; probe < cap; ++probe) {
       const uint32_t cur = *(volatile uint32_t *)&tk[h];
       if (cur == key) { atomicAdd(&tc[h], n); break; }
       if (cur != 0u) { h = (h + 1u) & (cap - 1u); continue; }
+      if (sm.dabort) break;
       const uint32_t old = atomicCAS(&tk[h], 0u, key);
       if (old == 0u || old == key) {
         atomicAdd(&tc[h], n);
@@ -1381,53 +1381,78 @@ __device__ __noinline__ DistinctRes distinct_topp(const Params &P, int row, cons
   return res;
 }
 
-// select_nth_eq over a row in global memory with 16-byte vector loads (aligned rows): warp w owns a
-// contiguous run of vectors; per-lane W-bit match masks, warp sums, then one warp rescans its run.
+// select_nth_eq over a row in global memory with 16-byte vector loads (aligned rows).  Pass 1 counts
+// the matches of every 32-vector block (kLdRow blocks in flight per warp) into blk[] (nblk <= cap
+// words of shared memory); warp 0 scans the block counts; one warp reloads the single block that
+// holds the c-th copy.  Returns kNoCut if the row has more blocks than blk holds (caller falls back).
+constexpr int kLdRow = 8;
 template <typename T>
-__device__ uint32_t select_nth_eq_row(const T *in, int V, uint32_t K, uint32_t c, TailSmem &sm) {
+__device__ uint32_t select_nth_eq_row(const T *in, int V, uint32_t K, uint32_t c, TailSmem &sm, uint32_t *blk,
+                                      int blk_cap, bool &ok) {
   using VT = typename Vec<T>::type;
   constexpr int W = Vec<T>::W;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const VT *pv = reinterpret_cast<const VT *>(in);
   const int nv = V / W;
-  const int seg = ((nv + kWarps - 1) / kWarps + 31) & ~31;
-  const int beg = warp * seg, end = min(nv, beg + seg);
+  const int nblk = (nv + 31) / 32;
+  ok = nblk <= blk_cap;
+  if (!ok) return kNoCut;  // uniform
   auto mask_of = [&](VT r) -> uint32_t {
     uint32_t mk = 0u;
 #pragma unroll
     for (int w = 0; w < W; ++w) mk |= (key_of_bits(lane_bits<T>(r, w)) == K ? 1u : 0u) << w;
     return mk;
   };
-  uint32_t cnt = 0u;
-  for (int base = beg; base < end; base += 32 * kLd) {
+  // pass 1: block b = 32 consecutive vectors; warp w takes blocks w, w + 8, ... (kLdRow at a time)
+  for (int b0 = warp; b0 < nblk; b0 += kWarps * kLdRow) {
+    uint32_t cnt[kLdRow];
 #pragma unroll
-    for (int j = 0; j < kLd; ++j) {
-      const int vi = base + 32 * j + lane;
-      if (vi < end) cnt += (uint32_t)__popc(mask_of(__ldcg(pv + vi)));
+    for (int j = 0; j < kLdRow; ++j) {
+      const int vi = (b0 + j * kWarps) * 32 + lane;
+      cnt[j] = vi < nv ? (uint32_t)__popc(mask_of(__ldcg(pv + vi))) : 0u;
+    }
+#pragma unroll
+    for (int j = 0; j < kLdRow; ++j) {
+      const uint32_t t = warp_sum(cnt[j]);
+      if (lane == 0 && b0 + j * kWarps < nblk) blk[b0 + j * kWarps] = t;
     }
   }
-  cnt = warp_sum(cnt);
-  if (lane == 0) sm.sel[warp] = cnt;
   tsync();
-  if (threadIdx.x == 0) {
-    uint32_t acc = 0u;
-    int w = 0;
-    for (; w < kWarps; ++w) {
-      if (acc + sm.sel[w] >= c) break;
-      acc += sm.sel[w];
+  // warp 0: first block whose inclusive prefix reaches c
+  if (warp == 0) {
+    const int per = (nblk + 31) / 32;
+    uint32_t loc = 0u;
+    for (int i = 0; i < per; ++i) {
+      const int b = lane * per + i;
+      if (b < nblk) loc += blk[b];
     }
-    sm.u[0] = (uint32_t)w;
-    sm.u[1] = c - acc;
-    sm.u[2] = kNoCut;
+    uint32_t incl = loc;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += t;
+    }
+    uint32_t before = incl - loc;
+    const bool mine = before < c && incl >= c;
+    const uint32_t who = __ballot_sync(0xffffffffu, mine);
+    if (mine) {
+      for (int i = 0; i < per; ++i) {
+        const int b = lane * per + i;
+        const uint32_t t = b < nblk ? blk[b] : 0u;
+        if (before + t >= c) { sm.u[0] = (uint32_t)b; sm.u[1] = c - before; break; }
+        before += t;
+      }
+    }
+    if (who == 0u && lane == 0) { sm.u[0] = 0xffffffffu; sm.u[1] = 0u; }
   }
   tsync();
-  if (warp == (int)sm.u[0]) {
-    uint32_t need = sm.u[1];
-    for (int base = beg; base < end; base += 32) {
-      const int vi = base + lane;
-      VT r;
-      uint32_t mk = 0u;
-      if (vi < end) { r = __ldcg(pv + vi); mk = mask_of(r); }
+  if (warp == 0) {
+    const uint32_t b = sm.u[0];
+    uint32_t res = kNoCut;
+    if (b != 0xffffffffu) {
+      const uint32_t need = sm.u[1];
+      const int vi = (int)b * 32 + lane;
+      const uint32_t mk = vi < nv ? mask_of(__ldcg(pv + vi)) : 0u;
       const uint32_t pc = (uint32_t)__popc(mk);
       uint32_t incl = pc;
 #pragma unroll
@@ -1435,13 +1460,10 @@ __device__ uint32_t select_nth_eq_row(const T *in, int V, uint32_t K, uint32_t c
         const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
         if (lane >= o) incl += t;
       }
-      const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
-      if (tot >= need) {
-        if (incl >= need && incl - pc < need) sm.u[2] = (uint32_t)(vi * W + nth_set_bit(mk, need - (incl - pc)));
-        break;
-      }
-      need -= tot;
+      if (incl >= need && incl - pc < need) res = (uint32_t)(vi * W + nth_set_bit(mk, need - (incl - pc)));
+      res = warp_min(res);
     }
+    if (lane == 0) sm.u[2] = res;
   }
   tsync();
   const uint32_t res = sm.u[2];
@@ -1763,7 +1785,13 @@ __device__ void tail_resolve(const Params &P, int row, const RowPlan &pl, uint32
   Red red(sm);
   // c-th copy of key K in index order (the duplicate-trimming rule of pipeline.py:53-56)
   auto row_select = [&](uint32_t K, uint32_t c) -> uint32_t {
-    return row_vec ? select_nth_eq_row<T>(in, V, K, c, sm) : select_nth_eq(RW, K, c, red);
+    if (row_vec) {  // block counts in the first 8 KB of the work area (free whenever a cut is selected)
+      bool ok;
+      const uint32_t r = select_nth_eq_row<T>(in, V, K, c, sm, reinterpret_cast<uint32_t *>(work),
+                                              2 * kNB, ok);
+      if (ok) return r;
+    }
+    return select_nth_eq(RW, K, c, red);
   };
   red.act_key = (uint32_t *)ap;  // the top-k search runs first: the whole region holds keys
   red.act_pi = ap;
