@@ -1828,6 +1828,7 @@ __device__ void tail_resolve(const Params &P, int row, const RowPlan &pl, uint32
   }
 
   // ================= top-p stage: pipeline.py:161-196 (p only) and :226-239 (k then p) ============
+  bool x_ok = true;  // X still holds the outliers
   // ================= top-p only over the whole row: distinct-value path =================
   if (!sorted_out && mode == MODE_TOPP && NP == 3 && !nodup && (!x_fits || sizeof(T) == 2)) {
     // table in X (2 x 4096 words); the kCapC probabilities behind the bin-sort layout when the work
@@ -1837,6 +1838,7 @@ __device__ void tail_resolve(const Params &P, int row, const RowPlan &pl, uint32
                          ? reinterpret_cast<double *>(work + kWorkBytesBins)
                          : reinterpret_cast<double *>(xb + 2 * cap);
     const DistinctRes dr = distinct_topp<T>(P, row, in, V, m, pl, xb, xb + cap, cap, cb, ci, db, di, hc, he, dev_pi, sm);
+    x_ok = false;  // the attempt used X's shared memory as its hash table
     if (dr.ok) {
       met.outlier_prob_sum = sigma ? dr.mx : 0.0;
       met.trunc_hit = (sigma && dr.hit && !force_fb) ? 1 : 0;
@@ -1854,6 +1856,7 @@ __device__ void tail_resolve(const Params &P, int row, const RowPlan &pl, uint32
     }
   }
   const bool distinct_done = sorted_out && mode == MODE_TOPP;
+  const bool x_fits_p = x_fits && x_ok;  // X as staged by the stream (top-p stage)
 
   if (!sorted_out && (mode == MODE_TOPP || mode == MODE_TOPKP)) {
     red.act_key = ak;  // (key, probability) pairs from here on
@@ -1911,7 +1914,7 @@ __device__ void tail_resolve(const Params &P, int row, const RowPlan &pl, uint32
       bool hit_ref = false;
       if (sigma) {
         Fx Mx;
-        if (x_fits) {
+        if (x_fits_p) {
           Mx = block_mass(X, [&](uint32_t b, uint32_t, int, double &v) { v = pi_bits(b); return true; }, cnt_dummy, red);
         } else {
           Mx = block_mass(RW, [&](uint32_t b, uint32_t, int, double &v) {
@@ -1923,7 +1926,7 @@ __device__ void tail_resolve(const Params &P, int row, const RowPlan &pl, uint32
       }
       met.trunc_hit = (hit_ref && !force_fb) ? 1 : 0;
       met.fallback_used = met.trunc_hit ? 0 : 1;
-      if (met.trunc_hit && x_fits) {
+      if (met.trunc_hit && x_fits_p) {
         set_kind = 1; l0 = pl.key_thr ? pl.key_thr - 1u : 0u;
       } else {
         set_kind = 2; l0 = lo_row;
@@ -2427,6 +2430,11 @@ __global__ void __launch_bounds__(kFusedThreads, 2) qrita_fused(Params P) {
     }
     {
       QRITA_TSTAMP(0);
+      if ((P.flags & QRITA_DEBUG_TIMING) && tid == 0) {  // debug: which SM ran the row
+        uint32_t smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        P.dbg[(size_t)row * 16 + 15] = smid;
+      }
       // (1) plan: the sample-independent part while the first stages land, then the sample in place
       if (tid == 32) { fs.n_x = 0u; plan_begin(P, row, &fs.pl); }  // warp 1, while warp 0 fills the ring
       const int ns = P.tree.n_leaves > 0 ? (P.tree.n + CE - 1) / CE : 0;

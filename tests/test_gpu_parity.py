@@ -221,3 +221,38 @@ def test_host_tensor_path(cuda_device):
     bad[20, 5] = float("nan")
     with pytest.raises(ValueError, match="NaN logit at row 20, col 5"):
         Q.topk_topp(bad, torch.from_numpy(k[:n]), torch.from_numpy(p[:n]))
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_random_sweep_fused_and_staged(cuda_device, seed):
+    """Randomised shapes / distributions / targets through both pipelines (fused for 16-byte-aligned
+    rows, staged otherwise and under QRITA_STAGED), fp32 and bf16, against the oracle."""
+    rng = np.random.default_rng(1000 + seed)
+    cases = []
+    for v in (4096, 5000, 33000, 65536, 100003):
+        for kind in ("normal", "ties", "wide", "spiky"):
+            b = 6
+            if kind == "normal":
+                x = rng.normal(size=(b, v))
+            elif kind == "ties":
+                x = np.round(rng.normal(size=(b, v)) * 3) / 3
+            elif kind == "wide":
+                x = rng.normal(size=(b, v)) * 30
+            else:  # a few huge logits on a gaussian bed (peaked distributions)
+                x = rng.normal(size=(b, v))
+                x[:, rng.integers(0, v, 5)] += 25.0
+            k = rng.integers(1, min(v, 3000) + 1, b)
+            k[0] = v  # top-p only
+            p = rng.choice([0.3, 0.8, 0.95, 0.999, 1.0], b)
+            cases.append((x.astype(np.float32), k, p))
+    for x, k, p in cases:
+        for dtype in (torch.float32, torch.bfloat16):
+            xs = x if dtype == torch.float32 else \
+                (to_bf16_bits(x).astype(np.uint32) << 16).view(np.float32)
+            for staged in (False, True):
+                out, kept, _ = run(xs, k, p, dtype=dtype, staged=staged)
+                for i in range(xs.shape[0]):
+                    keep = oracle_keep_row(xs[i], int(k[i]), float(p[i]))
+                    assert np.array_equal(~np.isneginf(out[i]), keep), (xs.shape, dtype, staged, i, k[i], p[i])
+                    assert kept[i] == keep.sum()
+                    assert np.array_equal(out[i][keep].view(np.uint32), xs[i][keep].view(np.uint32))

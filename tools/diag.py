@@ -179,3 +179,34 @@ if len(sys.argv) > 1 and sys.argv[1] == "ftiming":
         print("   row start percentiles", np.round(q, 1))
         q = np.percentile((end - t0) / 1e3, [0, 25, 50, 75, 100])
         print("   row end percentiles  ", np.round(q, 1))
+
+if len(sys.argv) > 1 and sys.argv[1] == "smid":
+    # fused kernel: stream time of rows on SMs that host one vs two rows
+    import bench, ctypes
+    from paper_2602_01518_b200 import _native as N
+    cfg = sys.argv[2] if len(sys.argv) > 2 else "cfg2"
+    x, k, p, dtype, desc = bench.workload(cfg)
+    xt = torch.from_numpy(x).cuda()
+    kt, pt = torch.from_numpy(k).cuda(), torch.from_numpy(p).cuda()
+    fl = Q.TruncFlags(debug_timing=True)
+    st = torch.cuda.current_stream()
+    for _ in range(3):
+        Q.topk_topp(xt, kt, pt, flags=fl)
+    ws = Q.ops.workspace_for(xt.device, st)
+    ptr, _ = ws.get(0, st)
+    B = x.shape[0]
+    for rep in range(3):
+        ws.buf.zero_()
+        Q.topk_topp(xt, kt, pt, flags=fl)
+        buf = (ctypes.c_ulonglong * (16 * B))()
+        N.load().qrita_get_timing(ctypes.c_void_p(ptr), B, buf, ctypes.c_void_p(st.cuda_stream))
+        a = np.frombuffer(buf, dtype=np.uint64).reshape(B, 16).astype(np.int64)
+        sm = a[:, 15]
+        cnt = np.bincount(sm, minlength=148)
+        per = cnt[sm]
+        stream = (a[:, 2] - a[:, 1]) / 1e3
+        end = (a[:, 9] - a[:, 0].min()) / 1e3
+        for n in (1, 2):
+            sel = per == n
+            if sel.any():
+                print(f"rep{rep} rows on {n}-row SMs: {sel.sum():3d}  stream mean {stream[sel].mean():6.2f} max {stream[sel].max():6.2f}  end mean {end[sel].mean():6.2f} max {end[sel].max():6.2f}")
