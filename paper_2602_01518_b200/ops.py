@@ -275,12 +275,11 @@ def _status_view(ws: Workspace, b: int) -> torch.Tensor:
 def topk_topp_host(logits: torch.Tensor, k, p, *, out: Optional[torch.Tensor] = None,
                    flags: Optional[TruncFlags] = None, sample_size: int = DEFAULT_SAMPLE_SIZE,
                    kept_count: Optional[torch.Tensor] = None, metrics: Optional[torch.Tensor] = None,
-                   check: bool = True, device=None, chunk_bytes: int = 8 << 20,
-                   n_streams: int = 3) -> torch.Tensor:
-    """topk_topp for a host [B, V] tensor: rows go to the GPU in chunks of ~chunk_bytes round-robin
-    over n_streams streams; on each stream a chunk is copied in, truncated, and copied back, so the
-    host-to-device and device-to-host transfers of different chunks overlap each other and the
-    kernels.  Pinned host memory gives asynchronous copies; pageable memory works, synchronously.
+                   check: bool = True, device=None, chunk_bytes: int = 16 << 20) -> torch.Tensor:
+    """topk_topp for a host [B, V] tensor.  Three streams: one uploads row chunks of ~chunk_bytes back
+    to back, one truncates each chunk as soon as it has landed, one downloads each result as soon
+    as it is ready, so both PCIe directions stay busy and overlap the kernels (per-chunk events
+    order them).  Pinned host memory gives asynchronous copies; pageable memory works, synchronously.
     Returns the masked logits as a host tensor (`out` when given).  kept_count / metrics, if given,
     are CUDA tensors.  check=True raises the reference's ValueError for invalid rows (after all
     chunks ran); the call always returns with the result in host memory."""
@@ -299,40 +298,63 @@ def topk_topp_host(logits: torch.Tensor, k, p, *, out: Optional[torch.Tensor] = 
         raise ValueError("out must be a contiguous host tensor matching logits")
     kt = _per_row(k, b, torch.int64, dev, "k")
     pt = _per_row(p, b, torch.float64, dev, "p")
-    rows = max(1, min(b, chunk_bytes // (v * logits.element_size())))
-    streams = _streams_for(dev, n_streams)
+    up, comp, down = _streams_for(dev, 3)
     cur = torch.cuda.current_stream(dev)
     status = torch.zeros((b,), dtype=torch.int32, device=dev)
-    nfcol = torch.full((b,), -1, dtype=torch.int32, device=dev)
     with torch.cuda.device(dev):
-        for s in streams:
-            s.wait_stream(cur)  # k / p / status were produced on the current stream
-        bufs = {}
-        for i, r0 in enumerate(range(0, b, rows)):
-            r1 = min(b, r0 + rows)
-            s = streams[i % n_streams]
-            with torch.cuda.stream(s):
-                if s not in bufs:
-                    bufs[s] = (torch.empty((rows, v), dtype=logits.dtype, device=dev),
-                               torch.empty((rows, v), dtype=logits.dtype, device=dev))
-                xd, od = bufs[s]
-                xd, od = xd[:r1 - r0], od[:r1 - r0]
-                xd.copy_(logits[r0:r1], non_blocking=True)
-                topk_topp(xd, kt[r0:r1], pt[r0:r1], out=od, flags=flags, sample_size=sample_size,
-                          kept_count=kept_count[r0:r1] if kept_count is not None else None,
-                          metrics=metrics[r0:r1] if metrics is not None else None,
-                          check=False, stream=s)
-                st, nf = _status_view(workspace_for(dev, s), r1 - r0)
-                status[r0:r1].copy_(st, non_blocking=True)
-                nfcol[r0:r1].copy_(nf, non_blocking=True)
-                out[r0:r1].copy_(od, non_blocking=True)
-                for t in (xd, od):
-                    t.record_stream(s)
-        for s in streams:
+        xd = torch.empty((b, v), dtype=logits.dtype, device=dev)
+        od = torch.empty((b, v), dtype=logits.dtype, device=dev)
+        for s in (up, comp, down):
+            s.wait_stream(cur)  # k / p / status / buffers were produced on the current stream
+        rows = max(1, min(b, chunk_bytes // (v * logits.element_size())))
+        spans = [(r0, min(b, r0 + rows)) for r0 in range(0, b, rows)]
+        landed, done = [], []
+        with torch.cuda.stream(up):
+            for r0, r1 in spans:
+                xd[r0:r1].copy_(logits[r0:r1], non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(up)
+                landed.append(ev)
+        with torch.cuda.stream(comp):
+            # lean per-chunk launches straight through the C ABI (arguments prepared once)
+            lib = N.load()
+            dt = _DTYPES[logits.dtype]
+            fl = (flags or TruncFlags()).bits()
+            esz = logits.element_size()
+            maxr = max(r1 - r0 for r0, r1 in spans)
+            ws = workspace_for(dev, comp)
+            ws_ptr, ws_bytes = ws.get(lib.qrita_workspace_bytes(maxr, v, dt, fl), comp)
+            st_all, _ = _status_view(ws, maxr)
+            x0, o0, k0, p0 = xd.data_ptr(), od.data_ptr(), kt.data_ptr(), pt.data_ptr()
+            kc0 = kept_count.data_ptr() if kept_count is not None else 0
+            me0 = metrics.data_ptr() if metrics is not None else 0
+            cs = ctypes.c_void_p(comp.cuda_stream)
+            for (r0, r1), ev in zip(spans, landed):
+                comp.wait_event(ev)
+                rc = lib.qrita_topk_topp(
+                    ctypes.c_void_p(x0 + r0 * v * esz), v, dt, r1 - r0, v,
+                    ctypes.c_void_p(k0 + 8 * r0), ctypes.c_void_p(p0 + 8 * r0),
+                    ctypes.c_void_p(o0 + r0 * v * esz), v,
+                    ctypes.c_void_p(kc0 + 4 * r0 if kc0 else 0),
+                    ctypes.c_void_p(me0 + N.METRICS_BYTES * r0 if me0 else 0),
+                    ctypes.c_void_p(ws_ptr), ws_bytes, fl, int(sample_size), cs)
+                if rc != N.OK:
+                    raise RuntimeError(f"qrita_topk_topp failed: {N.strerror(rc)}")
+                status[r0:r1].copy_(st_all[:r1 - r0], non_blocking=True)
+                ev2 = torch.cuda.Event()
+                ev2.record(comp)
+                done.append(ev2)
+        with torch.cuda.stream(down):
+            for (r0, r1), ev in zip(spans, done):
+                down.wait_event(ev)
+                out[r0:r1].copy_(od[r0:r1], non_blocking=True)
+        for s in (up, comp, down):
             cur.wait_stream(s)
+        for t in (xd, od, status):
+            for s in (up, comp, down):
+                t.record_stream(s)
         if check:
-            bad = status.ne(0)
-            if bool(bad.any()):  # synchronises
+            if bool(status.ne(0).any()):  # synchronises
                 raise TruncationError("invalid batch: " + "; ".join(
                     describe_invalid(logits, kt.cpu(), pt.cpu())[:5] or ["invalid rows"]))
         torch.cuda.synchronize(dev)

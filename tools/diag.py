@@ -210,3 +210,35 @@ if len(sys.argv) > 1 and sys.argv[1] == "smid":
             sel = per == n
             if sel.any():
                 print(f"rep{rep} rows on {n}-row SMs: {sel.sum():3d}  stream mean {stream[sel].mean():6.2f} max {stream[sel].max():6.2f}  end mean {end[sel].mean():6.2f} max {end[sel].max():6.2f}")
+
+if len(sys.argv) > 1 and sys.argv[1] == "smidmap":
+    # per-SM stream time over several runs: are slow rows tied to particular SMs?
+    import bench, ctypes
+    from paper_2602_01518_b200 import _native as N
+    x, k, p, dtype, desc = bench.workload("cfg2")
+    xt = torch.from_numpy(x).cuda()
+    kt, pt = torch.from_numpy(k).cuda(), torch.from_numpy(p).cuda()
+    fl = Q.TruncFlags(debug_timing=True)
+    st = torch.cuda.current_stream()
+    for _ in range(3):
+        Q.topk_topp(xt, kt, pt, flags=fl)
+    ws = Q.ops.workspace_for(xt.device, st)
+    ptr, _ = ws.get(0, st)
+    B = x.shape[0]
+    acc = np.zeros(148); n = np.zeros(148)
+    for rep in range(8):
+        ws.buf.zero_()
+        Q.topk_topp(xt, kt, pt, flags=fl)
+        buf = (ctypes.c_ulonglong * (16 * B))()
+        N.load().qrita_get_timing(ctypes.c_void_p(ptr), B, buf, ctypes.c_void_p(st.cuda_stream))
+        a = np.frombuffer(buf, dtype=np.uint64).reshape(B, 16).astype(np.int64)
+        sm = a[:, 15]
+        stream = (a[:, 2] - a[:, 1]) / 1e3
+        np.add.at(acc, sm, stream); np.add.at(n, sm, 1)
+    mean = acc / np.maximum(n, 1)
+    order = np.argsort(-mean)
+    print("slowest SMs (smid: mean stream us, rows):", [(int(i), round(mean[i], 1), int(n[i] / 8)) for i in order[:12]])
+    print("fastest SMs:", [(int(i), round(mean[i], 1), int(n[i] / 8)) for i in order[-8:]])
+    two = n / 8 == 2
+    print("2-row SMs: smid<74 mean", round(mean[two & (np.arange(148) < 74)].mean(), 2), " smid>=74 mean", round(mean[two & (np.arange(148) >= 74)].mean(), 2))
+    print("per-SM std over 2-row SMs", round(mean[two].std(), 2))
