@@ -2518,7 +2518,14 @@ static cudaError_t launch_fused(const Params &P, cudaStream_t st) {
     if (e != cudaSuccess) return e;
     grid_cap = sms * (per_sm < 1 ? 1 : per_sm);
   }
-  const int grid = P.B < grid_cap ? P.B : grid_cap;
+  // Balanced persistent grid: every CTA gets the same number of rows (no partial last wave), as
+  // long as that keeps >= 3/4 of the CTA slots (and their ring bytes in flight) busy.
+  int grid = P.B < grid_cap ? P.B : grid_cap;
+  if (P.B > grid_cap && !getenv("QRITA_UNBALANCED")) {
+    const int per = (P.B + grid_cap - 1) / grid_cap;
+    const int bal = (P.B + per - 1) / per;
+    if (4 * bal >= 3 * grid_cap) grid = bal;
+  }
   qrita_fused<T, NP><<<grid, kFusedThreads, kFusedDynSmem, st>>>(P);
   return cudaGetLastError();
 }
