@@ -256,3 +256,37 @@ def test_random_sweep_fused_and_staged(cuda_device, seed):
                     assert np.array_equal(~np.isneginf(out[i]), keep), (xs.shape, dtype, staged, i, k[i], p[i])
                     assert kept[i] == keep.sum()
                     assert np.array_equal(out[i][keep].view(np.uint32), xs[i][keep].view(np.uint32))
+
+
+def test_mixed_modes_many_rows_per_cta(cuda_device):
+    """700 rows (several per persistent CTA) mixing pass-through, top-k, top-p-only, top-k+top-p,
+    invalid k / p and non-finite rows: the ring's stage sequence runs across rows that take
+    different resolve paths; valid rows stay exact and the status names the first bad row."""
+    rng = np.random.default_rng(77)
+    b, v = 700, 8192
+    x = rng.normal(size=(b, v)).astype(np.float32)
+    x[::7] = np.round(x[::7] * 2) / 2  # tie-heavy rows
+    k = rng.integers(1, 2000, b)
+    p = rng.choice([0.4, 0.9, 0.999, 1.0], b)
+    mode = rng.integers(0, 4, b)
+    k[mode == 0] = v; p[mode == 0] = 1.0   # pass-through
+    k[mode == 1] = v                       # top-p only
+    p[mode == 2] = 1.0                     # top-k only
+    bad_k, bad_p, bad_nf = 101, 202, 303
+    k[bad_k] = v + 5
+    p[bad_p] = 0.0
+    x[bad_nf, 4321] = np.inf
+    xt = torch.from_numpy(x).cuda()
+    kept = torch.zeros(b, dtype=torch.int32, device="cuda")
+    out = Q.topk_topp(xt, torch.from_numpy(k).cuda(), torch.from_numpy(p).cuda(), kept_count=kept, check=False)
+    torch.cuda.synchronize()
+    got, kc = out.cpu().numpy(), kept.cpu().numpy()
+    for i in range(b):
+        if i in (bad_k, bad_p, bad_nf):
+            continue
+        keep = oracle_keep_row(x[i], int(k[i]), float(p[i]))
+        want = np.where(keep, x[i], -np.inf).astype(np.float32)
+        assert G.same_bits(got[i], want).all(), (i, k[i], p[i])
+        assert kc[i] == keep.sum(), i
+    with pytest.raises(ValueError, match="non-finite logit at row 303, col 4321"):
+        Q.topk_topp(xt, torch.from_numpy(k).cuda(), torch.from_numpy(p).cuda())
