@@ -1238,26 +1238,58 @@ __device__ __noinline__ DistinctRes distinct_topp(const Params &P, int row, cons
   for (int i = tid; i < kNB; i += kThreads) hc[i] = 0u;
   if (tid == 0) { sm.nd = 0u; sm.dabort = 0u; sm.u[4] = 0u; sm.dkmin = 0xffffffffu; sm.dkmax = 0u; }
   tsync();
-  // 1. count every distinct key (keys of finite logits are >= 1; 0 marks an empty slot)
-  for_row_warp<T>(in, V, [&](int, bool valid, uint32_t bits) {
-    if (!valid) return;
-    const uint32_t key = key_of_bits(bits);
-    const uint32_t n = 1u;  // per-lane atomics: cheaper than match_any aggregation here
+  // 1. count every distinct key (keys of finite logits are >= 1; 0 marks an empty slot).  Elements go
+  //    in batches: the table probes of a batch are independent loads, and keys already present (all
+  //    but the first copy of each value) take one atomic add; new keys go through the CAS insert.
+  auto insert_slow = [&](uint32_t key) {
     uint32_t h = (key * 0x9E3779B1u) >> (32u - lg);
     for (uint32_t probe = 0; probe < cap; ++probe) {
       const uint32_t cur = *(volatile uint32_t *)&tk[h];
-      if (cur == key) { atomicAdd(&tc[h], n); break; }
+      if (cur == key) { atomicAdd(&tc[h], 1u); return; }
       if (cur != 0u) { h = (h + 1u) & (cap - 1u); continue; }
-      if (sm.dabort) break;
+      if (sm.dabort) return;
       const uint32_t old = atomicCAS(&tk[h], 0u, key);
       if (old == 0u || old == key) {
-        atomicAdd(&tc[h], n);
+        atomicAdd(&tc[h], 1u);
         if (old == 0u && atomicAdd(&sm.nd, 1u) >= limit) sm.dabort = 1u;
-        break;
+        return;
       }
       h = (h + 1u) & (cap - 1u);
     }
-  });
+  };
+  {
+    using VT = typename Vec<T>::type;
+    constexpr int W = Vec<T>::W;
+    if (((uintptr_t)in % 16) == 0 && V % W == 0) {
+      const VT *pv = reinterpret_cast<const VT *>(in);
+      const int nv = V / W;
+      for (int v0 = tid; v0 < nv; v0 += kThreads * 2) {
+        VT r[2];
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+          if (v0 + j * kThreads < nv) r[j] = __ldcg(pv + v0 + j * kThreads);
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          if (v0 + j * kThreads >= nv) continue;
+          uint32_t key[W], h[W], cur[W];
+#pragma unroll
+          for (int w = 0; w < W; ++w) {
+            key[w] = key_of_bits(lane_bits<T>(r[j], w));
+            h[w] = (key[w] * 0x9E3779B1u) >> (32u - lg);
+          }
+#pragma unroll
+          for (int w = 0; w < W; ++w) cur[w] = *(volatile uint32_t *)&tk[h[w]];
+#pragma unroll
+          for (int w = 0; w < W; ++w) {
+            if (cur[w] == key[w]) atomicAdd(&tc[h[w]], 1u);
+            else insert_slow(key[w]);
+          }
+        }
+      }
+    } else {
+      for (int i = tid; i < V; i += kThreads) insert_slow(key_of_bits(Elem<T>::bits(in[i])));
+    }
+  }
   tsync();
   QRITA_TSTAMP(10);
   if (sm.dabort) return res;  // block-uniform
