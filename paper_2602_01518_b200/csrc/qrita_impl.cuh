@@ -20,6 +20,7 @@
 //                with programmatic dependent launch; outliers go through per-row HBM buffers.
 // Both share tail_resolve and compute bit-identical results.
 #pragma once
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdlib.h>
@@ -117,6 +118,39 @@ template <> __device__ __forceinline__ float4 neg_inf_vec<float>() {
 template <> __device__ __forceinline__ uint4 neg_inf_vec<uint16_t>() {
   return make_uint4(0xff80ff80u, 0xff80ff80u, 0xff80ff80u, 0xff80ff80u);
 }
+
+// Per-element comparison of a 128-bit vector against the logit whose order key is K, as bit masks
+// (bit w = element w): value order == key order for finite logits, and IEEE equality already treats
+// -0.0 == +0.0, so full-row passes compare values directly instead of converting every element to a
+// key (fp32 compares; packed bf16x2 compares for bf16).
+template <typename T> struct VecCmp;
+template <> struct VecCmp<float> {
+  float kv;
+  __device__ __forceinline__ explicit VecCmp(uint32_t K) { kv = __uint_as_float(bits_of_key(K)); }
+  __device__ __forceinline__ void masks(const float4 &v, uint32_t &gt, uint32_t &eq) const {
+    gt = (v.x > kv ? 1u : 0u) | (v.y > kv ? 2u : 0u) | (v.z > kv ? 4u : 0u) | (v.w > kv ? 8u : 0u);
+    eq = (v.x == kv ? 1u : 0u) | (v.y == kv ? 2u : 0u) | (v.z == kv ? 4u : 0u) | (v.w == kv ? 8u : 0u);
+  }
+};
+template <> struct VecCmp<uint16_t> {
+  __nv_bfloat162 k2;
+  __device__ __forceinline__ explicit VecCmp(uint32_t K) {
+    const uint32_t kb = bits_of_key(K) >> 16;
+    const uint32_t w = kb | (kb << 16);
+    k2 = *reinterpret_cast<const __nv_bfloat162 *>(&w);
+  }
+  __device__ __forceinline__ void masks(const uint4 &v, uint32_t &gt, uint32_t &eq) const {
+    const uint32_t wd[4] = {v.x, v.y, v.z, v.w};
+    gt = eq = 0u;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const __nv_bfloat162 x = *reinterpret_cast<const __nv_bfloat162 *>(&wd[i]);
+      const uint32_t g = __hgt2_mask(x, k2), e = __heq2_mask(x, k2);
+      gt |= ((g & 1u) | ((g >> 15) & 2u)) << (2 * i);
+      eq |= ((e & 1u) | ((e >> 15) & 2u)) << (2 * i);
+    }
+  }
+};
 
 // ------------------------------------------------------------------------------------------------
 // K0: per-row preparation (sigma_trunc.py:69-103; mode routing of pipeline.py:199-218)
@@ -1429,11 +1463,11 @@ __device__ uint32_t select_nth_eq_row(const T *in, int V, uint32_t K, uint32_t c
   const int nblk = (nv + 31) / 32;
   ok = nblk <= blk_cap;
   if (!ok) return kNoCut;  // uniform
+  const VecCmp<T> cmp(K);
   auto mask_of = [&](VT r) -> uint32_t {
-    uint32_t mk = 0u;
-#pragma unroll
-    for (int w = 0; w < W; ++w) mk |= (key_of_bits(lane_bits<T>(r, w)) == K ? 1u : 0u) << w;
-    return mk;
+    uint32_t gt, eq;
+    cmp.masks(r, gt, eq);
+    return eq;
   };
   // pass 1: block b = 32 consecutive vectors; warp w takes blocks w, w + 8, ... (kLdRow at a time)
   for (int b0 = warp; b0 < nblk; b0 += kWarps * kLdRow) {
@@ -1517,6 +1551,7 @@ __device__ void write_row(const T *in, T *out, int V, uint32_t K, uint32_t cut, 
     const VT *pi = reinterpret_cast<const VT *>(in);
     VT *po = reinterpret_cast<VT *>(out);
     const int nv = V / W;
+    const VecCmp<T> cmp(K);
     for (int v0 = threadIdx.x; v0 < nv; v0 += kThreads * kLd) {
       VT r[kLd];
 #pragma unroll
@@ -1526,22 +1561,33 @@ __device__ void write_row(const T *in, T *out, int V, uint32_t K, uint32_t cut, 
       for (int j = 0; j < kLd; ++j) {
         const int vi = v0 + j * kThreads;
         if (vi >= nv) continue;
-        VT o = r[j];
-        T *oe = reinterpret_cast<T *>(&o);
-        const T *ie = reinterpret_cast<const T *>(&r[j]);
-        bool any_kept = false, all_kept = true;
-#pragma unroll
-        for (int w = 0; w < W; ++w) {
-          const bool kp = kept_by(key_of_bits(Elem<T>::bits(ie[w])), (uint32_t)(vi * W + w), K, cut);
-          any_kept |= kp;
-          all_kept &= kp;
-          if (!kp) oe[w] = Elem<T>::neg_inf();
-        }
-        if (how == 1 || (how == 2 && !all_kept)) po[vi] = o;
-        else if (how == 0 && any_kept) {
+        uint32_t gt, eq;
+        cmp.masks(r[j], gt, eq);
+        uint32_t kp = gt;
+        if (eq) {  // the boundary value: copies up to index `cut` are kept
 #pragma unroll
           for (int w = 0; w < W; ++w)
-            if (kept_by(key_of_bits(Elem<T>::bits(ie[w])), (uint32_t)(vi * W + w), K, cut)) out[vi * W + w] = ie[w];
+            if (((eq >> w) & 1u) && (uint32_t)(vi * W + w) <= cut) kp |= 1u << w;
+        }
+        constexpr uint32_t kAll = (1u << W) - 1u;
+        const T *ie = reinterpret_cast<const T *>(&r[j]);
+        if (how == 0) {
+          if (kp) {
+#pragma unroll
+            for (int w = 0; w < W; ++w)
+              if ((kp >> w) & 1u) out[vi * W + w] = ie[w];
+          }
+        } else if (kp == kAll) {
+          if (how == 1) po[vi] = r[j];
+        } else if (kp == 0u) {
+          po[vi] = neg_inf_vec<T>();
+        } else {
+          VT o = r[j];
+          T *oe = reinterpret_cast<T *>(&o);
+#pragma unroll
+          for (int w = 0; w < W; ++w)
+            if (!((kp >> w) & 1u)) oe[w] = Elem<T>::neg_inf();
+          po[vi] = o;
         }
       }
     }
