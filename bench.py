@@ -114,7 +114,7 @@ class ClockSampler:
                         self.reasons.add(name)
             except Exception:
                 pass
-            time.sleep(0.002)
+            time.sleep(0.0005)
 
     def __enter__(self):
         if self.nv is not None:
@@ -133,6 +133,18 @@ class ClockSampler:
                     "samples": 0}
         return {"sm_mhz": float(statistics.median(self.samples)), "sm_max_mhz": self.max_mhz,
                 "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def cpu_model() -> str:
+    """The host CPU model (lscpu's 'Model name'), for the CPU baseline's record."""
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
 def cpu_baseline_oracle(x, k, p, rows: int, procs: int):
@@ -181,6 +193,7 @@ def run_reference(args):
         "config": {"workload": desc, "batch": int(x.shape[0]), "vocab": int(x.shape[1]),
                    "sample_rows_per_step": per_step},
         "cpu_baseline": {"value": value, "unit": "rows/s", "cores": procs, "kind": "port",
+                         "cpu_model": cpu_model(), "host_cores": os.cpu_count(),
                          "sample": f"{per_step} rows of {args.config} per step through "
                                    "oracle/qrita_oracle.py (numpy restatement of oracle.py:70-89), "
                                    f"{procs} processes"},
@@ -358,6 +371,7 @@ def main():
             procs = min(os.cpu_count() or 1, rows)
             val, wall = cpu_baseline_oracle(x_np, k_np, p_np, rows, procs)
             line["cpu_baseline"] = {"value": val, "unit": "rows/s", "cores": procs, "kind": "port",
+                                    "cpu_model": cpu_model(), "host_cores": os.cpu_count(),
                                     "sample": f"first {rows} rows of {args.config} through "
                                               "oracle/qrita_oracle.py (numpy restatement of "
                                               f"oracle.py:70-89), {procs} processes, {wall:.2f}s"}
