@@ -308,6 +308,10 @@ def main():
     if kind == "staged":
         roofline.update({"prep_ms": prep_ms, "tail_ms_serialised": tail_ms})
     launches_per_step = 1 if kind == "fused" else 3
+    # passes over the logits per row (qrita_row_metrics.row_passes): 1 = read once from HBM
+    met = Q.ops.metrics_buffer(b, dev)
+    Q.topk_topp(x, k, p, out=out, metrics=met, check=True)
+    passes = [m["row_passes"] for m in Q.ops.decode_metrics(met)]
 
     line = {
         "metric": METRIC, "value": value, "unit": "rows/s", "n_gpus": world, "steps": args.steps,
@@ -320,6 +324,7 @@ def main():
         "roofline": roofline,
         "clocks": clk.summary(),
         "gpu_launches": launches_per_step * args.steps,
+        "passes_over_logits": {"mean": sum(passes) / len(passes), "max": max(passes)},
         "pipeline": kind,
     }
 

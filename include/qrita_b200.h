@@ -81,7 +81,8 @@ typedef struct qrita_row_metrics {
   int32_t fallback_used;     /* reference semantics: not trunc_hit                            */
   int32_t kept_count;        /* number of kept entries                                        */
   int32_t full_row_path;     /* 1 if this build searched the full row (miss / capacity)       */
-  int32_t reserved;
+  int32_t row_passes;        /* passes over the row's logits: 1 = the single streaming pass; each   */
+                             /* full-row re-read of a fallback / full-row path adds one           */
 } qrita_row_metrics;
 
 /* Bytes of device workspace needed for a [B, V] call.  The workspace must be zeroed once before its

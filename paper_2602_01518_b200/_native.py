@@ -51,7 +51,7 @@ class RowMetricsC(ctypes.Structure):
         ("fallback_used", ctypes.c_int32),
         ("kept_count", ctypes.c_int32),
         ("full_row_path", ctypes.c_int32),
-        ("reserved", ctypes.c_int32),
+        ("row_passes", ctypes.c_int32),
     ]
 
 

@@ -194,9 +194,12 @@ __device__ __forceinline__ void pdl_launch_dependents() {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 
-// Barrier of the row-tail thread group: the first kThreads threads of the CTA (named barrier 1).
-// In the fused kernel the TMA producer warp is not part of it; in qrita_tail it is the whole CTA.
-__device__ __forceinline__ void tsync() { asm volatile("bar.sync 1, %0;" :: "n"(kThreads) : "memory"); }
+// Barrier of the row-tail thread group (named barrier 1, kThreads threads), in the non-aligned form
+// (`barrier.sync`; `bar.sync` is `barrier.sync.aligned`).  Callers reach it right after
+// thread-0-only branches and the compiler does not treat inline asm as a barrier, so a warp may
+// arrive diverged: undefined behaviour for the aligned form, and a deadlock was observed (even with
+// a __syncwarp() in front).  Measured: no cost on the hot path.
+__device__ __forceinline__ void tsync() { asm volatile("barrier.sync 1, %0;" :: "n"(kThreads) : "memory"); }
 
 // ------------------------------------------------------------------------------------------------
 // mbarrier / bulk-copy (TMA) primitives for the fused kernel's chunk ring

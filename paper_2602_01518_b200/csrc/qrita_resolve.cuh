@@ -458,6 +458,7 @@ __device__ void tail_resolve(const Params &P, int row, const RowPlan &pl, uint32
 
   qrita_row_metrics met;
   memset(&met, 0, sizeof(met));
+  if (tid == 0) sm.row_passes = 1u;  // the streaming pass; full-row re-reads below add to it
   if (nf_col != 0xffffffffu) {  // validate_batch (core.py:124-128): reported, row left undefined
     uint32_t first = 0xffffffffu;  // exact first non-finite column (error path only)
     for (int i = (int)nf_col + tid; i < V; i += kThreads)
@@ -477,6 +478,7 @@ __device__ void tail_resolve(const Params &P, int row, const RowPlan &pl, uint32
   if (mode == MODE_PASS) {  // _passthrough, pipeline.py:81-85 (the stream already copied the row)
     if (tid == 0) {
       met.kept_count = V;
+      met.row_passes = 1;
       if (P.kept_count) P.kept_count[row] = V;
       if (P.metrics) P.metrics[row] = met;
     }
@@ -674,8 +676,12 @@ __device__ void tail_resolve(const Params &P, int row, const RowPlan &pl, uint32
       bool ok;
       const uint32_t r = select_nth_eq_row<T>(in, V, K, c, sm, reinterpret_cast<uint32_t *>(work),
                                               2 * kNB, ok);
-      if (ok) return r;
+      if (ok) {
+        if (tid == 0) ++sm.row_passes;
+        return r;
+      }
     }
+    if (tid == 0) ++sm.row_passes;
     return select_nth_eq(RW, K, c, red);
   };
   red.act_key = (uint32_t *)ap;  // the top-k search runs first: the whole region holds keys
@@ -698,6 +704,7 @@ __device__ void tail_resolve(const Params &P, int row, const RowPlan &pl, uint32
       kr = search_k<NP>(X, pl.key_thr ? pl.key_thr - 1u : 0u, maxkey, n_c, 0u, k, red);
     } else {
       kr = search_k<NP>(RW, lo_row, maxkey, (uint32_t)V, 0u, k, red);
+      if (tid == 0) sm.row_passes += (uint32_t)kr.src_passes;
       full_row = true;
     }
     met.k_search_iters = kr.iters;
@@ -724,6 +731,7 @@ __device__ void tail_resolve(const Params &P, int row, const RowPlan &pl, uint32
                          : reinterpret_cast<double *>(xb + 2 * cap);
     const DistinctRes dr = distinct_topp<T>(P, row, in, V, m, pl, xb, xb + cap, cap, cb, ci, db, di, hc, he, dev_pi, sm);
     x_ok = false;  // the attempt used X's shared memory as its hash table
+    if (tid == 0) ++sm.row_passes;  // its counting pass read the whole row
     if (dr.ok) {
       met.outlier_prob_sum = sigma ? dr.mx : 0.0;
       met.trunc_hit = (sigma && dr.hit && !force_fb) ? 1 : 0;
@@ -781,6 +789,7 @@ __device__ void tail_resolve(const Params &P, int row, const RowPlan &pl, uint32
         v = e_of(b); return true; }, cnt_dummy, red);
       D = fx_to_double(Dx);
     } else {
+      if (tid == 0) ++sm.row_passes;
       const Fx Dx = block_mass(RW, [&](uint32_t b, uint32_t ix, int, double &v) {
         if (!in_s(key_of_bits(b), ix)) return false;
         v = e_of(b); return true; }, cnt_dummy, red);
@@ -802,6 +811,7 @@ __device__ void tail_resolve(const Params &P, int row, const RowPlan &pl, uint32
         if (x_fits_p) {
           Mx = block_mass(X, [&](uint32_t b, uint32_t, int, double &v) { v = pi_bits(b); return true; }, cnt_dummy, red);
         } else {
+          if (tid == 0) ++sm.row_passes;
           Mx = block_mass(RW, [&](uint32_t b, uint32_t, int, double &v) {
             if (key_of_bits(b) < pl.key_thr) return false;
             v = pi_bits(b); return true; }, cnt_dummy, red);
@@ -832,6 +842,7 @@ __device__ void tail_resolve(const Params &P, int row, const RowPlan &pl, uint32
       pr = search_p<NP>(X, l0, maxkey, Tp, Tsp, in_s, [&](uint32_t b, int) { return pi_bits(b); }, pi_key, red);
     } else {
       pr = search_p<NP>(RW, l0, maxkey, Tp, Tsp, in_s, [&](uint32_t b, int) { return pi_bits(b); }, pi_key, red);
+      if (tid == 0) sm.row_passes += (uint32_t)pr.src_passes;
     }
     if (pr.keep_all) {
       // p >= fsum(all survivors): keep them all (oracle.py:45-46)
@@ -867,6 +878,9 @@ __device__ void tail_resolve(const Params &P, int row, const RowPlan &pl, uint32
 
   QRITA_TSTAMP(8);
   // ================= output: finalize_mask, pipeline.py:60-78 =================
+  if (mode == MODE_TOPP || inplace || (!sorted_out && !k_used_x)) {
+    if (tid == 0) ++sm.row_passes;  // write_row reads the whole row again
+  }
   if (mode == MODE_TOPP) {
     write_row<T>(in, out, V, Kf, cutf, inplace ? 2 : 1);  // the stream left top-p-only rows alone
   } else if (inplace) {
@@ -885,6 +899,7 @@ __device__ void tail_resolve(const Params &P, int row, const RowPlan &pl, uint32
   if (tid == 0) {
     met.kept_count = (int32_t)kept;
     met.full_row_path = full_row ? 1 : 0;
+    met.row_passes = (int32_t)sm.row_passes;
     if (P.kept_count) P.kept_count[row] = (int32_t)kept;
     if (P.metrics) P.metrics[row] = met;
   }

@@ -32,6 +32,7 @@ struct TailSmem {
   uint32_t scan_u[kWarps];      // bin sort: warp totals of the bin-start scan
   Fx scan_f[2][kWarps];         // bin sort: warp totals of the two mass scans
   uint32_t bstar, nabove, bail, L;
+  uint32_t row_passes;          // full passes over the row's logits in this row's tail
   uint32_t nd, dabort, dK, dngt, dneq, dkmin, dkmax;  // distinct-value top-p
   uint32_t scan_u2[kWarps];
   Fx dH, dMx;
@@ -259,6 +260,7 @@ struct KRes {
   uint32_t n_gt;   // keys strictly above K
   uint32_t n_eq;   // keys equal to K
   int iters;
+  int src_passes;  // full passes over src (bracket, compaction, passes before compaction)
 };
 
 // Warp stage of a pivot pass: lane 0 of every warp stores the warp's bucket partials.
@@ -446,7 +448,9 @@ __device__ KRes search_k(const Src &src, uint32_t l, uint32_t r, uint32_t cl, ui
   }
   tsync();
   const Fx zero = fx_zero();
+  int sp = 0;  // full passes over src
   if (r - l > (uint32_t)(4 * kBins)) {
+    ++sp;
     bracket_pass<false>(src, [&](uint32_t, uint32_t) { return true; },
                         [&](uint32_t, int) { return 0.0; }, k, zero, R);
     if (threadIdx.x == 0 && !st.done) {
@@ -460,6 +464,7 @@ __device__ KRes search_k(const Src &src, uint32_t l, uint32_t r, uint32_t cl, ui
     l = st.l; r = st.r; cr = st.cr;
     if (st.done || r - l <= 1u) break;
     if (st.compact && !act) {
+      ++sp;
       // keep only the keys that can still matter: (l, r]  (order is irrelevant to counts)
       for_elems_warp(src, src.n, [&](int, bool valid, uint32_t bits, uint32_t) {
         const uint32_t key = key_of_bits(bits);
@@ -482,6 +487,7 @@ __device__ KRes search_k(const Src &src, uint32_t l, uint32_t r, uint32_t cl, ui
         if (key > piv[0] && key <= r) bk_add(b, piv, key, zero);
       }
     } else {
+      ++sp;
       for_elems(src, n, [&](int, uint32_t bits, uint32_t) {
         const uint32_t key = key_of_bits(bits);
         if (key > piv[0] && key <= r) bk_add(b, piv, key, zero);
@@ -525,13 +531,14 @@ __device__ KRes search_k(const Src &src, uint32_t l, uint32_t r, uint32_t cl, ui
     }
     tsync();
   }
-  const KRes res = st.done ? KRes{st.K, st.n_gt, st.n_eq, st.iters}
-                           : KRes{st.r, st.cr, st.cl - st.cr, st.iters};
+  const KRes res = st.done ? KRes{st.K, st.n_gt, st.n_eq, st.iters, sp}
+                           : KRes{st.r, st.cr, st.cl - st.cr, st.iters, sp};
   tsync();
   return res;
 }
 
 struct PRes {
+  int src_passes;  // full passes over src
   uint32_t K;      // boundary key of the nucleus
   uint32_t n_gt;   // survivors strictly above K
   uint32_t n_eq;   // survivors equal to K
@@ -550,6 +557,7 @@ template <int NP, class Src, class InS, class PiOf, class PiKey>
 __device__ PRes search_p(const Src &src, uint32_t l, uint32_t r, const Fx &T, const Fx &Tsp, InS in_s,
                          PiOf pi_of, PiKey pi_key, Red &R) {
   SearchState &st = R.sm.st;
+  int sp = 1;  // full passes over src: the bracketing pass or the total-mass pass, then below
   uint32_t cl = 0u, cr = 0u;
   Fx Ml = fx_zero(), Mr = fx_zero();
   if (threadIdx.x == 0) {
@@ -563,6 +571,7 @@ __device__ PRes search_p(const Src &src, uint32_t l, uint32_t r, const Fx &T, co
       PRes res{};
       res.keep_all = true;
       res.total = st.Ml;
+      res.src_passes = sp;
       tsync();
       return res;
     }
@@ -580,6 +589,7 @@ __device__ PRes search_p(const Src &src, uint32_t l, uint32_t r, const Fx &T, co
       PRes res{};
       res.keep_all = true;
       res.total = tot;
+      res.src_passes = sp;
       return res;
     }
     if (threadIdx.x == 0) { st.cl = cnt; st.Ml = tot; }
@@ -591,6 +601,7 @@ __device__ PRes search_p(const Src &src, uint32_t l, uint32_t r, const Fx &T, co
     if (st.done || r - l <= 1u) break;
     Mr = st.Mr;
     if (st.compact && !act) {
+      ++sp;
       // survivors in (l, r] with their probabilities: later passes need neither src nor exp()
       for_elems_warp(src, src.n, [&](int i, bool valid, uint32_t bits, uint32_t ix) {
         const uint32_t key = key_of_bits(bits);
@@ -612,6 +623,7 @@ __device__ PRes search_p(const Src &src, uint32_t l, uint32_t r, const Fx &T, co
         if (key > piv[0] && key <= r) bk_add(b, piv, key, fx_from_double(R.act_pi[i]));
       }
     } else {
+      ++sp;
       for_elems(src, n, [&](int i, uint32_t bits, uint32_t ix) {
         const uint32_t key = key_of_bits(bits);
         if (key > piv[0] && key <= r && in_s(key, ix)) bk_add(b, piv, key, fx_from_double(pi_of(bits, i)));
@@ -665,8 +677,8 @@ __device__ PRes search_p(const Src &src, uint32_t l, uint32_t r, const Fx &T, co
     }
     tsync();
   }
-  const PRes res = st.done ? PRes{st.K, st.n_gt, st.n_eq, st.H, st.iters, false, fx_zero()}
-                           : PRes{st.r, st.cr, st.cl - st.cr, st.Mr, st.iters, false, fx_zero()};
+  const PRes res = st.done ? PRes{sp, st.K, st.n_gt, st.n_eq, st.H, st.iters, false, fx_zero()}
+                           : PRes{sp, st.r, st.cr, st.cl - st.cr, st.Mr, st.iters, false, fx_zero()};
   tsync();
   return res;
 }

@@ -290,3 +290,15 @@ def test_mixed_modes_many_rows_per_cta(cuda_device):
         assert kc[i] == keep.sum(), i
     with pytest.raises(ValueError, match="non-finite logit at row 303, col 4321"):
         Q.topk_topp(xt, torch.from_numpy(k).cuda(), torch.from_numpy(p).cuda())
+
+
+def test_row_passes_metric(cuda_device):
+    """qrita_row_metrics.row_passes: the fused bin-sort path reads each logit once; full-row paths
+    (forced fallback, top-p-only rows) report their extra passes."""
+    x, k, p, dtype, trip, _ = G.config("cfg2")
+    _, _, met = run(x[:32], k[:32], p[:32])
+    assert all(m["row_passes"] == 1 for m in met)
+    _, _, met = run(x[:4], k[:4], p[:4], force_fallback=True)
+    assert all(m["row_passes"] > 1 for m in met)
+    _, _, met = run(x[:4], np.full(4, x.shape[1]), np.full(4, 1.0))
+    assert all(m["row_passes"] == 1 for m in met)

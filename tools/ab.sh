@@ -1,4 +1,2 @@
-for v in p q p q; do QRITA_LIB=build/ab/$v.so timeout 300 python bench.py --no-extras --steps 30 > gpurun_out/ab_$v.log 2>&1; python -c "
+for v in p q r p q r; do QRITA_LIB=build/ab/$v.so timeout 300 python bench.py --no-extras --steps 30 > gpurun_out/ab_$v.log 2>&1; python -c "
 import json; d=json.loads(open('gpurun_out/ab_$v.log').read().strip().splitlines()[-1]); print('$v cfg2', round(d['ms_per_step']*1e3,2))" >> gpurun_out/ab.txt; done
-for v in p q; do QRITA_LIB=build/ab/$v.so timeout 300 python bench.py --config cfg3 --no-extras --steps 20 > gpurun_out/ab3_$v.log 2>&1; python -c "
-import json; d=json.loads(open('gpurun_out/ab3_$v.log').read().strip().splitlines()[-1]); print('$v cfg3', round(d['ms_per_step']*1e3,2))" >> gpurun_out/ab.txt; done
