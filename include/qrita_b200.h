@@ -121,6 +121,27 @@ int qrita_topk_topp_ex(const void *logits, int64_t ld_in, int dtype, int B, int 
                        void *workspace, size_t ws_bytes, int flags, int sample_size,
                        qrita_stream_t stream, void *prep_done_event, void *stream_done_event);
 
+/*
+ * Host-buffer variant (the reference's run_batch takes host arrays, engine.py:82-113): logits / out
+ * are HOST [B, V] row-major arrays (page-locked memory lets the copies run asynchronously), k / p are
+ * HOST arrays.  Row chunks of `chunk_rows` rows are copied in, truncated and copied back on three
+ * streams owned by the library (upload / truncate / download), ordered by per-chunk events, so both
+ * PCIe directions and the kernels overlap.  `scratch` is a DEVICE buffer of
+ * qrita_host_scratch_bytes(B, V, dtype, chunk_rows) bytes, 256-byte aligned (no initialisation
+ * needed).  The work is ordered after everything already enqueued on `stream`, and `stream` waits
+ * for all of it: synchronise `stream` before reading `out`.  kept_count / metrics: DEVICE or NULL.
+ * Invalid rows are reported by qrita_get_status_host.
+ */
+size_t qrita_host_scratch_bytes(int B, int V, int dtype, int chunk_rows);
+int qrita_topk_topp_host(const void *logits_host, int dtype, int B, int V,
+                         const int64_t *k_host, const double *p_host, void *out_host,
+                         int32_t *kept_count, qrita_row_metrics *metrics,
+                         void *scratch, size_t scratch_bytes, int chunk_rows, int flags, int sample_size,
+                         qrita_stream_t stream);
+/* qrita_get_status for the last qrita_topk_topp_host call on `scratch` (same B, V, chunk_rows). */
+int qrita_get_status_host(const void *scratch, int B, int V, int dtype, int chunk_rows, int *row, int *col,
+                          qrita_stream_t stream);
+
 /* Synchronises `stream`, then reports the first failing row of the last call on this workspace:
  * returns QRITA_OK or QRITA_EINVAL_K / QRITA_EINVAL_P / QRITA_ENONFINITE, and fills *row / *col
  * (col = first non-finite column, or -1). */

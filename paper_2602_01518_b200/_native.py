@@ -34,8 +34,8 @@ ENCCL = 7
 
 EXPORTED_SYMBOLS = (
     "qrita_workspace_bytes", "qrita_workspace_init", "qrita_topk_topp", "qrita_topk_topp_ex",
-    "qrita_get_status", "qrita_get_timing",
-    "qrita_strerror", "qrita_version",
+    "qrita_get_status", "qrita_get_timing", "qrita_host_scratch_bytes", "qrita_topk_topp_host",
+    "qrita_get_status_host", "qrita_strerror", "qrita_version",
 )
 
 
@@ -88,6 +88,12 @@ def load() -> ctypes.CDLL:
     lib.qrita_get_status.restype = i32
     lib.qrita_get_timing.argtypes = [vp, i32, vp, vp]
     lib.qrita_get_timing.restype = i32
+    lib.qrita_host_scratch_bytes.argtypes = [i32, i32, i32, i32]
+    lib.qrita_host_scratch_bytes.restype = sz
+    lib.qrita_topk_topp_host.argtypes = [vp, i32, i32, i32, vp, vp, vp, vp, vp, vp, sz, i32, i32, i32, vp]
+    lib.qrita_topk_topp_host.restype = i32
+    lib.qrita_get_status_host.argtypes = [vp, i32, i32, i32, i32, ctypes.POINTER(i32), ctypes.POINTER(i32), vp]
+    lib.qrita_get_status_host.restype = i32
     lib.qrita_strerror.argtypes = [i32]
     lib.qrita_strerror.restype = ctypes.c_char_p
     lib.qrita_version.argtypes = []

@@ -1,10 +1,12 @@
 // qrita_capi.cu — the extern "C" entry points of libqrita_b200.so (include/qrita_b200.h).
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdio.h>
 #include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
+#include <mutex>
 #include <vector>
 
 #include "qrita_types.cuh"
@@ -70,6 +72,61 @@ void pw_tree(int n, PwTree &t) {
   t.n_levels = (int16_t)levels;
 }
 
+// Host-buffer pipeline (qrita_topk_topp_host): scratch = [chunk workspaces | k | p | in | out].
+// Equal chunks of R rows (the last one shorter).  A ramp (small first / last chunks) was measured
+// and lost: every copy has a fixed cost and both PCIe directions run at ~42 GB/s when busy together.
+std::vector<std::pair<int, int>> host_chunks(int B, int R) {
+  std::vector<std::pair<int, int>> ch;
+  for (int r0 = 0; r0 < B; r0 += R) ch.push_back({r0, std::min(R, B - r0)});
+  return ch;
+}
+
+struct HostLayout {
+  int nchunks;
+  std::vector<std::pair<int, int>> chunks;  // (first row, rows)
+  size_t ws_each, st, nf, k, p, in, out, total;
+};
+
+HostLayout host_layout(int B, int V, int dtype, int chunk_rows) {
+  HostLayout H;
+  const size_t es = dtype == QRITA_DTYPE_F32 ? 4 : 2;
+  H.chunks = host_chunks(B, chunk_rows);
+  H.nchunks = (int)H.chunks.size();
+  H.ws_each = align_up(ws_layout(chunk_rows, V).total, 256);
+  size_t off = H.ws_each * (size_t)H.nchunks;
+  H.st = off;  off = align_up(off + 4ull * (size_t)B, 256);
+  H.nf = off;  off = align_up(off + 4ull * (size_t)B, 256);
+  H.k = off;   off = align_up(off + 8ull * (size_t)B, 256);
+  H.p = off;   off = align_up(off + 8ull * (size_t)B, 256);
+  H.in = off;  off = align_up(off + es * (size_t)B * (size_t)V, 256);
+  H.out = off; off = align_up(off + es * (size_t)B * (size_t)V, 256);
+  H.total = off;
+  return H;
+}
+
+// The library's own streams and a growing event pool, per device; one host-buffer call enqueues at a
+// time (the events are reused across calls, so the enqueue section is serialised).
+struct HostPipe {
+  cudaStream_t up = nullptr, comp = nullptr, down = nullptr;
+  std::vector<cudaEvent_t> ev;
+};
+std::mutex g_host_mu;
+HostPipe g_host_pipe[64];
+
+cudaError_t host_pipe_get(int dev, size_t nev, HostPipe *&hp) {
+  if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
+  hp = &g_host_pipe[dev];
+  cudaError_t e = cudaSuccess;
+  for (cudaStream_t *s : {&hp->up, &hp->comp, &hp->down})
+    if (!*s && (e = cudaStreamCreateWithFlags(s, cudaStreamNonBlocking)) != cudaSuccess) return e;
+  while (hp->ev.size() < nev) {
+    cudaEvent_t x;
+    if ((e = cudaEventCreateWithFlags(&x, cudaEventDisableTiming)) != cudaSuccess) return e;
+    hp->ev.push_back(x);
+  }
+  return cudaSuccess;
+}
+
 }  // namespace
 
 extern "C" {
@@ -94,11 +151,16 @@ int qrita_topk_topp(const void *logits, int64_t ld_in, int dtype, int B, int V,
                             workspace, ws_bytes, flags, sample_size, stream, NULL, NULL);
 }
 
-int qrita_topk_topp_ex(const void *logits, int64_t ld_in, int dtype, int B, int V,
-                       const int64_t *k, const double *p, void *out, int64_t ld_out,
-                       int32_t *kept_count, qrita_row_metrics *metrics,
-                       void *workspace, size_t ws_bytes, int flags, int sample_size,
-                       qrita_stream_t stream, void *prep_done_event, void *stream_done_event) {
+}  // extern "C"
+
+namespace {
+
+// qrita_topk_topp_ex with the status / nf_col words optionally placed outside the workspace (the
+// host-buffer pipeline gathers the chunks' status into one [B] block).
+int topk_topp_impl(const void *logits, int64_t ld_in, int dtype, int B, int V, const int64_t *k, const double *p,
+                   void *out, int64_t ld_out, int32_t *kept_count, qrita_row_metrics *metrics, void *workspace,
+                   size_t ws_bytes, int flags, int sample_size, qrita_stream_t stream, void *prep_done_event,
+                   void *stream_done_event, int32_t *status, int32_t *nf_col) {
   if (!logits || !out || !k || !p || !workspace) return QRITA_EINVAL_ARG;
   if (B < 1 || V < 1 || ld_in < V || ld_out < V || sample_size < 1) return QRITA_EINVAL_ARG;
   if (dtype != QRITA_DTYPE_F32 && dtype != QRITA_DTYPE_BF16) return QRITA_EINVAL_ARG;
@@ -123,8 +185,8 @@ int qrita_topk_topp_ex(const void *logits, int64_t ld_in, int dtype, int B, int 
   P.agg = (RowAgg *)(ws + L.agg);
   P.cand_bits = (uint32_t *)(ws + L.cand_bits);
   P.cand_idx = (uint32_t *)(ws + L.cand_idx);
-  P.status = (int32_t *)(ws + L.status);
-  P.nf_col = (int32_t *)(ws + L.nf_col);
+  P.status = status ? status : (int32_t *)(ws + L.status);
+  P.nf_col = nf_col ? nf_col : (int32_t *)(ws + L.nf_col);
   P.dbg = (unsigned long long *)(ws + L.dbg);
   P.nchunks = (int)nchunks;
   P.xcap = row_cap(V);
@@ -142,34 +204,147 @@ int qrita_topk_topp_ex(const void *logits, int64_t ld_in, int dtype, int B, int 
   return e == cudaSuccess ? QRITA_OK : QRITA_ECUDA;
 }
 
-int qrita_get_status(const void *workspace, int B, int *row, int *col, qrita_stream_t stream) {
-  if (!workspace || B < 1) return QRITA_EINVAL_ARG;
-  if (cudaStreamSynchronize((cudaStream_t)stream) != cudaSuccess) return QRITA_ECUDA;
-  const WsLayout L = ws_layout(B, 1);  // status block offsets depend on B only
-  const uint8_t *ws = (const uint8_t *)workspace;
-  int32_t *st = (int32_t *)malloc(sizeof(int32_t) * 2 * (size_t)B);
-  if (!st) return QRITA_EINVAL_ARG;
-  if (cudaMemcpy(st, ws + L.status, sizeof(int32_t) * (size_t)B, cudaMemcpyDeviceToHost) != cudaSuccess ||
-      cudaMemcpy(st + B, ws + L.nf_col, sizeof(int32_t) * (size_t)B, cudaMemcpyDeviceToHost) != cudaSuccess) {
-    free(st);
-    return QRITA_ECUDA;
-  }
-  int code = QRITA_OK;
+// First failing row of a [status[B] | nf_col[B]] pair in host memory (precedence: non-finite, k, p).
+int scan_status(const int32_t *st, const int32_t *nf, int B, int *row, int *col) {
   if (row) *row = -1;
   if (col) *col = -1;
-  for (int pass = 0; pass < 3 && code == QRITA_OK; ++pass) {
+  for (int pass = 0; pass < 3; ++pass) {
     const int bit = pass == 0 ? ST_NONFINITE : pass == 1 ? ST_BAD_K : ST_BAD_P;
     for (int r = 0; r < B; ++r) {
       if (st[r] & bit) {
-        code = pass == 0 ? QRITA_ENONFINITE : pass == 1 ? QRITA_EINVAL_K : QRITA_EINVAL_P;
         if (row) *row = r;
-        if (col) *col = pass == 0 ? st[B + r] : -1;
-        break;
+        if (col) *col = pass == 0 ? nf[r] : -1;
+        return pass == 0 ? QRITA_ENONFINITE : pass == 1 ? QRITA_EINVAL_K : QRITA_EINVAL_P;
       }
     }
   }
-  free(st);
-  return code;
+  return QRITA_OK;
+}
+
+int read_status(const int32_t *st_dev, const int32_t *nf_dev, int B, int *row, int *col, qrita_stream_t stream) {
+  if (cudaStreamSynchronize((cudaStream_t)stream) != cudaSuccess) return QRITA_ECUDA;
+  std::vector<int32_t> st(2 * (size_t)B);
+  if (cudaMemcpy(st.data(), st_dev, sizeof(int32_t) * (size_t)B, cudaMemcpyDeviceToHost) != cudaSuccess ||
+      cudaMemcpy(st.data() + B, nf_dev, sizeof(int32_t) * (size_t)B, cudaMemcpyDeviceToHost) != cudaSuccess)
+    return QRITA_ECUDA;
+  return scan_status(st.data(), st.data() + B, B, row, col);
+}
+
+}  // namespace
+
+extern "C" {
+
+int qrita_topk_topp_ex(const void *logits, int64_t ld_in, int dtype, int B, int V,
+                       const int64_t *k, const double *p, void *out, int64_t ld_out,
+                       int32_t *kept_count, qrita_row_metrics *metrics,
+                       void *workspace, size_t ws_bytes, int flags, int sample_size,
+                       qrita_stream_t stream, void *prep_done_event, void *stream_done_event) {
+  return topk_topp_impl(logits, ld_in, dtype, B, V, k, p, out, ld_out, kept_count, metrics, workspace, ws_bytes,
+                        flags, sample_size, stream, prep_done_event, stream_done_event, NULL, NULL);
+}
+
+size_t qrita_host_scratch_bytes(int B, int V, int dtype, int chunk_rows) {
+  if (B < 1 || V < 1 || chunk_rows < 1) return 0;
+  return host_layout(B, V, dtype, chunk_rows < B ? chunk_rows : B).total;
+}
+
+int qrita_topk_topp_host(const void *logits_host, int dtype, int B, int V,
+                         const int64_t *k_host, const double *p_host, void *out_host,
+                         int32_t *kept_count, qrita_row_metrics *metrics,
+                         void *scratch, size_t scratch_bytes, int chunk_rows, int flags, int sample_size,
+                         qrita_stream_t stream) {
+  if (!logits_host || !out_host || !k_host || !p_host || !scratch) return QRITA_EINVAL_ARG;
+  if (B < 1 || V < 1 || chunk_rows < 1 || sample_size < 1) return QRITA_EINVAL_ARG;
+  if (dtype != QRITA_DTYPE_F32 && dtype != QRITA_DTYPE_BF16) return QRITA_EINVAL_ARG;
+  if (flags & (QRITA_INPLACE | QRITA_DEBUG_TIMING)) return QRITA_EINVAL_ARG;
+  if (chunk_rows > B) chunk_rows = B;
+  const HostLayout H = host_layout(B, V, dtype, chunk_rows);
+  if (scratch_bytes < H.total || ((uintptr_t)scratch & 255u)) return QRITA_EWORKSPACE;
+  const size_t es = dtype == QRITA_DTYPE_F32 ? 4 : 2;
+  const size_t row_bytes = es * (size_t)V;
+  uint8_t *sc = (uint8_t *)scratch;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return QRITA_ECUDA;
+  std::lock_guard<std::mutex> lock(g_host_mu);
+  HostPipe *hp = nullptr;
+  const size_t nc = (size_t)H.nchunks;
+  if (host_pipe_get(dev, 2 * nc + 4, hp) != cudaSuccess) return QRITA_ECUDA;
+  cudaEvent_t *landed = hp->ev.data(), *done = landed + nc, *ev0 = done + nc;
+  const cudaStream_t caller = (cudaStream_t)stream;
+  auto ok = [](cudaError_t e) { return e == cudaSuccess; };
+  // QRITA_HOST_TRACE: timing events per chunk (uploaded / truncated / downloaded), printed to stderr
+  const bool trace = getenv("QRITA_HOST_TRACE") != NULL;
+  std::vector<cudaEvent_t> tr(trace ? 3 * nc + 1 : 0);
+  for (auto &x : tr) cudaEventCreate(&x);
+  if (trace) cudaEventRecord(tr[3 * nc], caller);
+  // everything already on the caller's stream (buffers, kept_count / metrics) comes first
+  // ... and so does the previous host-buffer call on these streams (its buffers may be this call's):
+  // ev0[1] still holds its last download (a never-recorded event is complete)
+  if (!ok(cudaEventRecord(ev0[0], caller))) return QRITA_ECUDA;
+  for (cudaStream_t s : {hp->up, hp->comp, hp->down})
+    if (!ok(cudaStreamWaitEvent(s, ev0[0], 0)) || !ok(cudaStreamWaitEvent(s, ev0[1], 0))) return QRITA_ECUDA;
+  // chunk workspaces start clean (one memset, overlapping the first upload)
+  if (!ok(cudaMemsetAsync(sc, 0, H.ws_each * nc, hp->comp))) return QRITA_ECUDA;
+  if (!ok(cudaMemcpyAsync(sc + H.k, k_host, 8ull * (size_t)B, cudaMemcpyHostToDevice, hp->up)) ||
+      !ok(cudaMemcpyAsync(sc + H.p, p_host, 8ull * (size_t)B, cudaMemcpyHostToDevice, hp->up)))
+    return QRITA_ECUDA;
+  for (size_t c = 0; c < nc; ++c) {
+    const size_t r0 = (size_t)H.chunks[c].first, nr = (size_t)H.chunks[c].second;
+    if (!ok(cudaMemcpyAsync(sc + H.in + r0 * row_bytes, (const uint8_t *)logits_host + r0 * row_bytes,
+                            nr * row_bytes, cudaMemcpyHostToDevice, hp->up)) ||
+        !ok(cudaEventRecord(landed[c], hp->up)))
+      return QRITA_ECUDA;
+    if (trace) cudaEventRecord(tr[c], hp->up);
+  }
+  for (size_t c = 0; c < nc; ++c) {
+    const size_t r0 = (size_t)H.chunks[c].first, nr = (size_t)H.chunks[c].second;
+    if (!ok(cudaStreamWaitEvent(hp->comp, landed[c], 0))) return QRITA_ECUDA;
+    const int rc = topk_topp_impl(sc + H.in + r0 * row_bytes, V, dtype, (int)nr, V,
+                                  (const int64_t *)(sc + H.k) + r0, (const double *)(sc + H.p) + r0,
+                                  sc + H.out + r0 * row_bytes, V, kept_count ? kept_count + r0 : NULL,
+                                  metrics ? metrics + r0 : NULL, sc + c * H.ws_each, H.ws_each, flags, sample_size,
+                                  (qrita_stream_t)hp->comp, NULL, NULL, (int32_t *)(sc + H.st) + r0,
+                                  (int32_t *)(sc + H.nf) + r0);
+    if (rc != QRITA_OK) return rc;
+    if (trace) cudaEventRecord(tr[nc + c], hp->comp);
+    if (!ok(cudaEventRecord(done[c], hp->comp)) || !ok(cudaStreamWaitEvent(hp->down, done[c], 0)) ||
+        !ok(cudaMemcpyAsync((uint8_t *)out_host + r0 * row_bytes, sc + H.out + r0 * row_bytes, nr * row_bytes,
+                            cudaMemcpyDeviceToHost, hp->down)))
+      return QRITA_ECUDA;
+    if (trace) cudaEventRecord(tr[2 * nc + c], hp->down);
+  }
+  if (trace) {
+    cudaDeviceSynchronize();
+    for (size_t c = 0; c < nc; ++c) {
+      float a = 0, b = 0, d = 0;
+      cudaEventElapsedTime(&a, tr[3 * nc], tr[c]);
+      cudaEventElapsedTime(&b, tr[3 * nc], tr[nc + c]);
+      cudaEventElapsedTime(&d, tr[3 * nc], tr[2 * nc + c]);
+      fprintf(stderr, "chunk %zu: up %.3f  kernel %.3f  down %.3f ms\n", c, a, b, d);
+    }
+    for (auto &x : tr) cudaEventDestroy(x);
+  }
+  // the caller's stream waits for the downloads and the last kernel (kept_count / metrics)
+  if (!ok(cudaEventRecord(ev0[1], hp->down)) || !ok(cudaEventRecord(ev0[2], hp->comp)) ||
+      !ok(cudaEventRecord(ev0[3], hp->up)) || !ok(cudaStreamWaitEvent(caller, ev0[1], 0)) ||
+      !ok(cudaStreamWaitEvent(caller, ev0[2], 0)) || !ok(cudaStreamWaitEvent(caller, ev0[3], 0)))
+    return QRITA_ECUDA;
+  return QRITA_OK;
+}
+
+int qrita_get_status_host(const void *scratch, int B, int V, int dtype, int chunk_rows, int *row, int *col,
+                          qrita_stream_t stream) {
+  if (!scratch || B < 1 || V < 1 || chunk_rows < 1) return QRITA_EINVAL_ARG;
+  const HostLayout H = host_layout(B, V, dtype, chunk_rows < B ? chunk_rows : B);
+  const uint8_t *sc = (const uint8_t *)scratch;
+  return read_status((const int32_t *)(sc + H.st), (const int32_t *)(sc + H.nf), B, row, col, stream);
+}
+
+int qrita_get_status(const void *workspace, int B, int *row, int *col, qrita_stream_t stream) {
+  if (!workspace || B < 1) return QRITA_EINVAL_ARG;
+  const WsLayout L = ws_layout(B, 1);  // status block offsets depend on B only
+  const uint8_t *ws = (const uint8_t *)workspace;
+  return read_status((const int32_t *)(ws + L.status), (const int32_t *)(ws + L.nf_col), B, row, col, stream);
 }
 
 int qrita_get_timing(const void *workspace, int B, unsigned long long *out, qrita_stream_t stream) {

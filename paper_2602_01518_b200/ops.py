@@ -246,43 +246,34 @@ def decode_metrics(buf: torch.Tensor):
 
 
 # ------------------------------------------------------------------------------------------------
-# Host buffers: chunked, overlapped transfers
+# Host buffers: chunked, overlapped transfers (the pipeline itself is native: qrita_topk_topp_host)
 # ------------------------------------------------------------------------------------------------
 _host_lock = threading.Lock()
-_host_streams = {}
+_host_scratch = {}
+DEFAULT_HOST_CHUNK_BYTES = 16 << 20  # measured best on cfg2 (tools/e2e_sweep.py)
 
 
-def _streams_for(device: torch.device, n: int):
-    key = (device.index, n)
+def _scratch_for(device: torch.device, nbytes: int) -> torch.Tensor:
+    """Per-device device scratch of the host-buffer pipeline, grown on demand (256-byte aligned)."""
     with _host_lock:
-        ss = _host_streams.get(key)
-        if ss is None:
-            ss = [torch.cuda.Stream(device) for _ in range(n)]
-            _host_streams[key] = ss
-        return ss
-
-
-def _status_view(ws: Workspace, b: int) -> torch.Tensor:
-    """The [status[b] | nf_col[b]] words at the head of a workspace (include/qrita_b200.h layout)."""
-    base = ws.buf.data_ptr()
-    off = ((base + 255) & ~255) - base
-    nf_off = off + ((4 * b + 255) // 256) * 256
-    st = ws.buf[off:off + 4 * b].view(torch.int32)
-    nf = ws.buf[nf_off:nf_off + 4 * b].view(torch.int32)
-    return st, nf
+        buf = _host_scratch.get(device.index)
+        if buf is None or buf.numel() < nbytes + 256:
+            buf = torch.empty(nbytes + 256, dtype=torch.uint8, device=device)
+            _host_scratch[device.index] = buf
+        return buf
 
 
 def topk_topp_host(logits: torch.Tensor, k, p, *, out: Optional[torch.Tensor] = None,
                    flags: Optional[TruncFlags] = None, sample_size: int = DEFAULT_SAMPLE_SIZE,
                    kept_count: Optional[torch.Tensor] = None, metrics: Optional[torch.Tensor] = None,
-                   check: bool = True, device=None, chunk_bytes: int = 16 << 20) -> torch.Tensor:
-    """topk_topp for a host [B, V] tensor.  Three streams: one uploads row chunks of ~chunk_bytes back
-    to back, one truncates each chunk as soon as it has landed, one downloads each result as soon
-    as it is ready, so both PCIe directions stay busy and overlap the kernels (per-chunk events
-    order them).  Pinned host memory gives asynchronous copies; pageable memory works, synchronously.
-    Returns the masked logits as a host tensor (`out` when given).  kept_count / metrics, if given,
-    are CUDA tensors.  check=True raises the reference's ValueError for invalid rows (after all
-    chunks ran); the call always returns with the result in host memory."""
+                   check: bool = True, device=None, chunk_bytes: int = DEFAULT_HOST_CHUNK_BYTES) -> torch.Tensor:
+    """topk_topp for a host [B, V] tensor through qrita_topk_topp_host: the library copies row chunks
+    of ~chunk_bytes in, truncates each as soon as it has landed and copies it back, on three streams
+    of its own, so both PCIe directions stay busy and overlap the kernels.  Pinned host memory gives
+    asynchronous copies; pageable memory works, with the copies staged synchronously by CUDA.
+    Returns the masked logits as a host tensor (`out` when given); the call returns with the result in
+    host memory.  kept_count / metrics, if given, are CUDA tensors.  check=True raises the
+    reference's ValueError for invalid rows."""
     if logits.dim() != 2:
         raise ValueError("logit batch must be 2-D (rows x vocab)")
     if logits.dtype not in _DTYPES:
@@ -291,71 +282,46 @@ def topk_topp_host(logits: torch.Tensor, k, p, *, out: Optional[torch.Tensor] = 
     b, v = logits.shape
     if b == 0 or v == 0:
         raise ValueError("batch_size and vocab_size must be >= 1")
+    if sample_size < 1:
+        raise ValueError("sample_size must be >= 1")
     dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
     if out is None:
         out = torch.empty_like(logits, pin_memory=logits.is_pinned())
     elif out.shape != logits.shape or out.dtype != logits.dtype or out.is_cuda or not out.is_contiguous():
         raise ValueError("out must be a contiguous host tensor matching logits")
-    kt = _per_row(k, b, torch.int64, dev, "k")
-    pt = _per_row(p, b, torch.float64, dev, "p")
-    up, comp, down = _streams_for(dev, 3)
-    cur = torch.cuda.current_stream(dev)
-    status = torch.zeros((b,), dtype=torch.int32, device=dev)
+    cpu = torch.device("cpu")
+    kt = _per_row(k, b, torch.int64, cpu, "k")
+    pt = _per_row(p, b, torch.float64, cpu, "p")
+    for t, nm in ((kept_count, "kept_count"), (metrics, "metrics")):
+        if t is not None and (not t.is_cuda or t.device != dev or not t.is_contiguous()):
+            raise ValueError(f"{nm} must be a contiguous CUDA tensor on {dev}")
+    lib = N.load()
+    dt = _DTYPES[logits.dtype]
+    fl = (flags or TruncFlags()).bits()
+    rows = max(1, min(b, chunk_bytes // (v * logits.element_size())))
+    need = lib.qrita_host_scratch_bytes(b, v, dt, rows)
     with torch.cuda.device(dev):
-        xd = torch.empty((b, v), dtype=logits.dtype, device=dev)
-        od = torch.empty((b, v), dtype=logits.dtype, device=dev)
-        for s in (up, comp, down):
-            s.wait_stream(cur)  # k / p / status / buffers were produced on the current stream
-        rows = max(1, min(b, chunk_bytes // (v * logits.element_size())))
-        spans = [(r0, min(b, r0 + rows)) for r0 in range(0, b, rows)]
-        landed, done = [], []
-        with torch.cuda.stream(up):
-            for r0, r1 in spans:
-                xd[r0:r1].copy_(logits[r0:r1], non_blocking=True)
-                ev = torch.cuda.Event()
-                ev.record(up)
-                landed.append(ev)
-        with torch.cuda.stream(comp):
-            # lean per-chunk launches straight through the C ABI (arguments prepared once)
-            lib = N.load()
-            dt = _DTYPES[logits.dtype]
-            fl = (flags or TruncFlags()).bits()
-            esz = logits.element_size()
-            maxr = max(r1 - r0 for r0, r1 in spans)
-            ws = workspace_for(dev, comp)
-            ws_ptr, ws_bytes = ws.get(lib.qrita_workspace_bytes(maxr, v, dt, fl), comp)
-            st_all, _ = _status_view(ws, maxr)
-            x0, o0, k0, p0 = xd.data_ptr(), od.data_ptr(), kt.data_ptr(), pt.data_ptr()
-            kc0 = kept_count.data_ptr() if kept_count is not None else 0
-            me0 = metrics.data_ptr() if metrics is not None else 0
-            cs = ctypes.c_void_p(comp.cuda_stream)
-            for (r0, r1), ev in zip(spans, landed):
-                comp.wait_event(ev)
-                rc = lib.qrita_topk_topp(
-                    ctypes.c_void_p(x0 + r0 * v * esz), v, dt, r1 - r0, v,
-                    ctypes.c_void_p(k0 + 8 * r0), ctypes.c_void_p(p0 + 8 * r0),
-                    ctypes.c_void_p(o0 + r0 * v * esz), v,
-                    ctypes.c_void_p(kc0 + 4 * r0 if kc0 else 0),
-                    ctypes.c_void_p(me0 + N.METRICS_BYTES * r0 if me0 else 0),
-                    ctypes.c_void_p(ws_ptr), ws_bytes, fl, int(sample_size), cs)
-                if rc != N.OK:
-                    raise RuntimeError(f"qrita_topk_topp failed: {N.strerror(rc)}")
-                status[r0:r1].copy_(st_all[:r1 - r0], non_blocking=True)
-                ev2 = torch.cuda.Event()
-                ev2.record(comp)
-                done.append(ev2)
-        with torch.cuda.stream(down):
-            for (r0, r1), ev in zip(spans, done):
-                down.wait_event(ev)
-                out[r0:r1].copy_(od[r0:r1], non_blocking=True)
-        for s in (up, comp, down):
-            cur.wait_stream(s)
-        for t in (xd, od, status):
-            for s in (up, comp, down):
-                t.record_stream(s)
+        st = torch.cuda.current_stream(dev)
+        buf = _scratch_for(dev, need)
+        base = buf.data_ptr()
+        sp = (base + 255) & ~255
+        rc = lib.qrita_topk_topp_host(
+            ctypes.c_void_p(logits.data_ptr()), dt, b, v, ctypes.c_void_p(kt.data_ptr()),
+            ctypes.c_void_p(pt.data_ptr()), ctypes.c_void_p(out.data_ptr()),
+            ctypes.c_void_p(kept_count.data_ptr() if kept_count is not None else 0),
+            ctypes.c_void_p(metrics.data_ptr() if metrics is not None else 0),
+            ctypes.c_void_p(sp), buf.numel() - (sp - base), rows, fl, int(sample_size),
+            ctypes.c_void_p(st.cuda_stream))
+        if rc != N.OK:
+            raise RuntimeError(f"qrita_topk_topp_host failed: {N.strerror(rc)}")
         if check:
-            if bool(status.ne(0).any()):  # synchronises
+            row, col = ctypes.c_int(-1), ctypes.c_int(-1)
+            code = lib.qrita_get_status_host(ctypes.c_void_p(sp), b, v, dt, rows, ctypes.byref(row),
+                                             ctypes.byref(col), ctypes.c_void_p(st.cuda_stream))
+            if code in (N.ENONFINITE, N.EINVAL_K, N.EINVAL_P):
                 raise TruncationError("invalid batch: " + "; ".join(
-                    describe_invalid(logits, kt.cpu(), pt.cpu())[:5] or ["invalid rows"]))
-        torch.cuda.synchronize(dev)
+                    describe_invalid(logits, kt, pt)[:5] or [N.strerror(code)]))
+            if code != N.OK:
+                raise RuntimeError(f"qrita_get_status_host failed: {N.strerror(code)}")
+        st.synchronize()
     return out

@@ -208,10 +208,11 @@ def test_outlier_spill_rows(cuda_device):
 
 
 def test_host_tensor_path(cuda_device):
-    """Host tensors in, host tensors out: chunked transfers overlapped over several streams
-    (ops.topk_topp_host); per-chunk status is gathered so errors still name the global row."""
+    """Host tensors in, host tensors out: chunked transfers overlapped over the library's three
+    streams (qrita_topk_topp_host); the chunks' status words land in one block, so errors still
+    name the global row."""
     x, k, p, dtype, trip, _ = G.config("cfg2")
-    n = 40  # 8 MB chunks of 16 rows -> 3 chunks over 3 streams
+    n = 40  # 16 MB chunks of 32 rows -> 2 chunks
     xh = torch.from_numpy(np.ascontiguousarray(x[:n])).pin_memory()
     kept = torch.zeros(n, dtype=torch.int32, device="cuda")
     out = Q.topk_topp(xh, torch.from_numpy(k[:n]), torch.from_numpy(p[:n]), kept_count=kept)
@@ -221,6 +222,45 @@ def test_host_tensor_path(cuda_device):
     bad[20, 5] = float("nan")
     with pytest.raises(ValueError, match="NaN logit at row 20, col 5"):
         Q.topk_topp(bad, torch.from_numpy(k[:n]), torch.from_numpy(p[:n]))
+
+
+@pytest.mark.parametrize("dtype,pinned,chunk_rows", [(torch.float32, False, 7), (torch.bfloat16, True, 3),
+                                                     (torch.float32, True, 1000)])
+def test_host_path_chunking(cuda_device, dtype, pinned, chunk_rows):
+    """qrita_topk_topp_host: pageable and pinned buffers, chunk sizes that do not divide B (and one
+    larger than B), bf16, kept counts and metrics offset per chunk, precedence of row errors."""
+    x, k, p, _, trip, _ = G.config("cfg2")
+    n = 23
+    xs = x[:n] if dtype == torch.float32 else torch.from_numpy(x[:n]).to(torch.bfloat16).float().numpy()
+    xh = torch.from_numpy(np.ascontiguousarray(x[:n])).to(dtype)
+    if pinned:
+        xh = xh.pin_memory()
+    kept = torch.zeros(n, dtype=torch.int32, device="cuda")
+    met = Q.ops.metrics_buffer(n, "cuda")
+    cb = chunk_rows * x.shape[1] * xh.element_size()
+    out = Q.ops.topk_topp_host(xh, torch.from_numpy(k[:n]), torch.from_numpy(p[:n]), kept_count=kept,
+                               metrics=met, chunk_bytes=cb)
+    assert not out.is_cuda and out.dtype == dtype
+    kc = kept.cpu().numpy()
+    if dtype == torch.float32:
+        assert_rows(x[:n], out.numpy(), kc, trip[:n], "host chunks")
+    else:
+        for r in range(n):
+            ref = oracle_keep_row(xs[r], int(k[r]), float(p[r]))
+            got = np.isfinite(out[r].float().numpy())
+            assert np.array_equal(got, ref), f"bf16 host row {r}"
+            assert kc[r] == ref.sum()
+    rows = Q.ops.decode_metrics(met)
+    assert [m["kept_count"] for m in rows] == list(kc)
+    # k error in a late chunk, NaN in an earlier one: non-finite wins (core.py:120-140 order)
+    bad = xh.clone()
+    bad[4, 9] = float("nan")
+    kb = torch.from_numpy(k[:n]).clone()
+    kb[20] = 0
+    with pytest.raises(ValueError, match="NaN logit at row 4, col 9"):
+        Q.ops.topk_topp_host(bad, kb, torch.from_numpy(p[:n]), chunk_bytes=cb)
+    with pytest.raises(ValueError, match="row 20"):
+        Q.ops.topk_topp_host(xh, kb, torch.from_numpy(p[:n]), chunk_bytes=cb)
 
 
 @pytest.mark.parametrize("seed", [0, 1, 2])
@@ -302,3 +342,32 @@ def test_row_passes_metric(cuda_device):
     assert all(m["row_passes"] > 1 for m in met)
     _, _, met = run(x[:4], np.full(4, x.shape[1]), np.full(4, 1.0))
     assert all(m["row_passes"] == 1 for m in met)
+
+
+def test_capi_host_numpy_binding(cuda_device):
+    """The INTEGRATION.md ctypes binding of qrita_topk_topp_host on plain (pageable) numpy arrays."""
+    import ctypes
+    from paper_2602_01518_b200 import _native as N
+    lib = N.load()
+    x, k, p, _, trip, _ = G.config("cfg2")
+    n = 20
+    xs = np.ascontiguousarray(x[:n]); out = np.empty_like(xs)
+    kk = np.ascontiguousarray(k[:n], np.int64); pp = np.ascontiguousarray(p[:n], np.float64)
+    B, V = xs.shape
+    rows = 6
+    nbytes = lib.qrita_host_scratch_bytes(B, V, 0, rows)
+    scratch = torch.empty(nbytes + 256, dtype=torch.uint8, device="cuda")
+    sp = (scratch.data_ptr() + 255) & ~255
+    st = torch.cuda.current_stream().cuda_stream
+    rc = lib.qrita_topk_topp_host(xs.ctypes.data, 0, B, V, kk.ctypes.data, pp.ctypes.data, out.ctypes.data,
+                                  None, None, sp, nbytes, rows, 0, 4096, st)
+    assert rc == N.OK
+    row, col = ctypes.c_int(), ctypes.c_int()
+    assert lib.qrita_get_status_host(sp, B, V, 0, rows, ctypes.byref(row), ctypes.byref(col), st) == N.OK
+    kept = np.isfinite(out).sum(axis=1).astype(np.int32)
+    assert_rows(xs, out, kept, trip[:n], "numpy host binding")
+    # too-small scratch and bad arguments are rejected before any work is enqueued
+    assert lib.qrita_topk_topp_host(xs.ctypes.data, 0, B, V, kk.ctypes.data, pp.ctypes.data, out.ctypes.data,
+                                    None, None, sp, nbytes - 1, rows, 0, 4096, st) == N.EWORKSPACE
+    assert lib.qrita_topk_topp_host(xs.ctypes.data, 0, B, V, kk.ctypes.data, pp.ctypes.data, out.ctypes.data,
+                                    None, None, sp, nbytes, 0, 0, 4096, st) == N.EINVAL_ARG

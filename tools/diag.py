@@ -155,13 +155,15 @@ if len(sys.argv) > 1 and sys.argv[1] == "ftiming":
         ptr, _ = ws.get(0, st)
         B = x.shape[0]
         ws.buf.zero_()
+        if os.environ.get("FLUSH"):  # evict the kernel's code and data from L2 first (serving-like)
+            fl_buf = torch.empty(64 << 20, device="cuda"); fl_buf.zero_(); fl_buf.sum()
         Q.topk_topp(xt, kt, pt, flags=fl)
         buf = (ctypes.c_ulonglong * (16 * B))()
         N.load().qrita_get_timing(ctypes.c_void_p(ptr), B, buf, ctypes.c_void_p(st.cuda_stream))
         a = np.frombuffer(buf, dtype=np.uint64).reshape(B, 16).astype(np.int64)
         t0 = a[:, 0].min()
         end = np.where(a[:, 9] > 0, a[:, 9], a[:, 2])
-        print(f"{cfg}: B={B} start spread {(a[:,0].max()-t0)/1e3:.1f} us, last end {(end.max()-t0)/1e3:.1f} us")
+        print(f"{cfg}: B={B} flush={bool(os.environ.get('FLUSH'))} start spread {(a[:,0].max()-t0)/1e3:.1f} us, last end {(end.max()-t0)/1e3:.1f} us")
         for nm, i, j in (("plan", 0, 1), ("stream", 1, 2), ("resolve", 2, 9)):
             ok = (a[:, i] > 0) & (a[:, j] > 0)
             d = (a[ok, j] - a[ok, i]) / 1e3

@@ -8,7 +8,9 @@ x_np, k_np, p_np, dtype, desc = bench.workload("cfg2")
 xh = torch.from_numpy(x_np).pin_memory(); oh = torch.empty_like(xh).pin_memory()
 kh, ph = torch.from_numpy(k_np), torch.from_numpy(p_np)
 st = torch.cuda.current_stream()
-for cb in (4 << 20, 8 << 20, 16 << 20, 32 << 20):
+for cb in (8 << 20, 16 << 20, 32 << 20):
+  for ramp in ("1", "0"):
+    os.environ["QRITA_HOST_RAMP"] = ramp
     for ns in (3,):
         ts = []
         for i in range(6):
@@ -20,4 +22,4 @@ for cb in (4 << 20, 8 << 20, 16 << 20, 32 << 20):
             torch.cuda.synchronize()
             if i >= 2:
                 ts.append(e0.elapsed_time(e1))
-        print(f"chunk {cb >> 20:3d} MB streams {ns}: {statistics.mean(ts):.3f} ms")
+        print(f"chunk {cb >> 20:3d} MB ramp {ramp}: {statistics.mean(ts):.3f} ms (min {min(ts):.3f})")
