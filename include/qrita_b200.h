@@ -110,6 +110,19 @@ int qrita_topk_topp(const void *logits, int64_t ld_in, int dtype, int B, int V,
                     void *workspace, size_t ws_bytes, int flags, int sample_size,
                     qrita_stream_t stream);
 
+/* qrita_topk_topp plus the kept-column list (SURVEY.md 8b kept_idx): kept_idx DEVICE int32 [B, ld_idx]
+ * (ld_idx >= V) receives each row's kept column indices in unspecified order, kept_count[row] of them
+ * (kept_count or metrics must be given).  out may be NULL: index-only output, no masked logits are
+ * written (V * sizeof(dtype) read + kept * 4 written per row).  Same validation and status as
+ * qrita_topk_topp; QRITA_INPLACE requires out. */
+int qrita_topk_topp_idx(const void *logits, int64_t ld_in, int dtype, int B, int V,
+                        const int64_t *k, const double *p,
+                        void *out, int64_t ld_out,
+                        int32_t *kept_idx, int64_t ld_idx,
+                        int32_t *kept_count, qrita_row_metrics *metrics,
+                        void *workspace, size_t ws_bytes, int flags, int sample_size,
+                        qrita_stream_t stream);
+
 /* Same as qrita_topk_topp, for profiling: records `prep_done_event` after the preparation kernel and
  * `stream_done_event` after the streaming kernel (cudaEvent_t each, may be NULL).  A non-NULL event
  * serialises the launches around it (no programmatic overlap), so each kernel can be timed alone

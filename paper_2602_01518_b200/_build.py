@@ -49,7 +49,8 @@ def build(verbose: bool = False, force: bool = False) -> str:
         o = os.path.join(BUILD_DIR, src.replace(".cu", ".o"))
         objs.append(o)
         if force or _stale(o, [s] + headers):
-            cmd = [nvcc, *ARCH, *NVCC_FLAGS, "-c", s, "-o", o]
+            # QRITA_NVCC_EXTRA: extra flags for A/B builds (e.g. -DQRITA_L2_PREFETCH=0; use force=True)
+            cmd = [nvcc, *ARCH, *NVCC_FLAGS, *os.environ.get("QRITA_NVCC_EXTRA", "").split(), "-c", s, "-o", o]
             if verbose:
                 cmd.insert(1, "-Xptxas=-v")
             jobs.append(cmd)

@@ -33,7 +33,7 @@ ECUDA = 6
 ENCCL = 7
 
 EXPORTED_SYMBOLS = (
-    "qrita_workspace_bytes", "qrita_workspace_init", "qrita_topk_topp", "qrita_topk_topp_ex",
+    "qrita_workspace_bytes", "qrita_workspace_init", "qrita_topk_topp", "qrita_topk_topp_ex", "qrita_topk_topp_idx",
     "qrita_get_status", "qrita_get_timing", "qrita_host_scratch_bytes", "qrita_topk_topp_host",
     "qrita_get_status_host", "qrita_strerror", "qrita_version",
 )
@@ -84,6 +84,9 @@ def load() -> ctypes.CDLL:
     lib.qrita_topk_topp_ex.argtypes = [vp, i64, i32, i32, i32, vp, vp, vp, i64, vp, vp, vp, sz, i32, i32,
                                        vp, vp, vp]
     lib.qrita_topk_topp_ex.restype = i32
+    lib.qrita_topk_topp_idx.argtypes = [vp, i64, i32, i32, i32, vp, vp, vp, i64, vp, i64, vp, vp, vp, sz, i32, i32,
+                                        vp]
+    lib.qrita_topk_topp_idx.restype = i32
     lib.qrita_get_status.argtypes = [vp, i32, ctypes.POINTER(i32), ctypes.POINTER(i32), vp]
     lib.qrita_get_status.restype = i32
     lib.qrita_get_timing.argtypes = [vp, i32, vp, vp]

@@ -160,8 +160,15 @@ namespace {
 int topk_topp_impl(const void *logits, int64_t ld_in, int dtype, int B, int V, const int64_t *k, const double *p,
                    void *out, int64_t ld_out, int32_t *kept_count, qrita_row_metrics *metrics, void *workspace,
                    size_t ws_bytes, int flags, int sample_size, qrita_stream_t stream, void *prep_done_event,
-                   void *stream_done_event, int32_t *status, int32_t *nf_col) {
-  if (!logits || !out || !k || !p || !workspace) return QRITA_EINVAL_ARG;
+                   void *stream_done_event, int32_t *status, int32_t *nf_col, int32_t *kept_idx = NULL,
+                   int64_t ld_idx = 0) {
+  if (!logits || !k || !p || !workspace) return QRITA_EINVAL_ARG;
+  if (!out && !kept_idx) return QRITA_EINVAL_ARG;
+  if (kept_idx && (ld_idx < V || (!kept_count && !metrics))) return QRITA_EINVAL_ARG;
+  if (!out) {
+    if (flags & QRITA_INPLACE) return QRITA_EINVAL_ARG;
+    ld_out = V;
+  }
   if (B < 1 || V < 1 || ld_in < V || ld_out < V || sample_size < 1) return QRITA_EINVAL_ARG;
   if (dtype != QRITA_DTYPE_F32 && dtype != QRITA_DTYPE_BF16) return QRITA_EINVAL_ARG;
   if (flags & ~(QRITA_SEARCH_BINARY | QRITA_NO_SIGMA | QRITA_FORCE_FALLBACK | QRITA_NO_DUP | QRITA_INPLACE |
@@ -181,6 +188,7 @@ int topk_topp_impl(const void *logits, int64_t ld_in, int dtype, int B, int V, c
   P.logits = logits; P.ld_in = ld_in; P.out = out; P.ld_out = ld_out;
   P.B = B; P.V = V; P.dtype = dtype; P.flags = flags; P.sample_size = sample_size;
   P.k = k; P.p = p; P.kept_count = kept_count; P.metrics = metrics;
+  P.kept_idx = kept_idx; P.ld_idx = ld_idx;
   P.plans = (RowPlan *)(ws + L.plans);
   P.agg = (RowAgg *)(ws + L.agg);
   P.cand_bits = (uint32_t *)(ws + L.cand_bits);
@@ -241,6 +249,14 @@ int qrita_topk_topp_ex(const void *logits, int64_t ld_in, int dtype, int B, int 
                        qrita_stream_t stream, void *prep_done_event, void *stream_done_event) {
   return topk_topp_impl(logits, ld_in, dtype, B, V, k, p, out, ld_out, kept_count, metrics, workspace, ws_bytes,
                         flags, sample_size, stream, prep_done_event, stream_done_event, NULL, NULL);
+}
+
+int qrita_topk_topp_idx(const void *logits, int64_t ld_in, int dtype, int B, int V, const int64_t *k,
+                        const double *p, void *out, int64_t ld_out, int32_t *kept_idx, int64_t ld_idx,
+                        int32_t *kept_count, qrita_row_metrics *metrics, void *workspace, size_t ws_bytes,
+                        int flags, int sample_size, qrita_stream_t stream) {
+  return topk_topp_impl(logits, ld_in, dtype, B, V, k, p, out, ld_out, kept_count, metrics, workspace, ws_bytes,
+                        flags, sample_size, stream, NULL, NULL, NULL, NULL, kept_idx, ld_idx);
 }
 
 size_t qrita_host_scratch_bytes(int B, int V, int dtype, int chunk_rows) {

@@ -239,6 +239,14 @@ __device__ __forceinline__ void tma_load_1d(void *dst, const void *src, uint32_t
   asm volatile("cp.async.bulk.shared::cta.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
                :: "r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy) : "memory");
 }
+// 16-byte streaming store of one 32-bit word repeated four times (the -inf background: one register).
+__device__ __forceinline__ void st_cs_splat4(void *p, uint32_t w) {
+  asm volatile("st.global.cs.v4.b32 [%0], {%1, %1, %1, %1};" :: "l"(p), "r"(w) : "memory");
+}
+// Bulk prefetch of global memory into L2 (no shared memory, no completion tracking).
+__device__ __forceinline__ void l2_prefetch_bulk(const void *src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" :: "l"(src), "r"(bytes) : "memory");
+}
 __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }

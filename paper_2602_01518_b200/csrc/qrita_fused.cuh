@@ -35,6 +35,10 @@ namespace qrita {
 constexpr int kStageBytes = 4096;
 constexpr int kCapXF = 5632;
 constexpr int kRing = 15;
+#ifndef QRITA_L2_PREFETCH
+#define QRITA_L2_PREFETCH 0  // measured neutral on cfg2 / cfg4 (tools/ab2.sh); kept as an option
+#endif
+
 constexpr int kFusedThreads = kThreads;  // 8 warps: stream, plan and resolve (no producer warp)
 static_assert(kRing >= 8, "ring must hold the sigma sample (<= 6 stages) plus slack");
 static_assert(kRing * kStageBytes >= kWorkBytes, "the ring doubles as the tail work area");
@@ -110,11 +114,15 @@ __device__ __forceinline__ void consume_chunk(const uint8_t *stage, int c0, int 
         m |= (M)(x1 >= thr) << (u * W + w + 1);
       }
     }
+    // one branch per chunk; lane-based pointer with immediate offsets; -inf from one register
+    VT *pd = reinterpret_cast<VT *>(dst) + lane;
+    if (write_bg) {
+      const uint32_t ni = sizeof(T) == 4 ? 0xff800000u : 0xff80ff80u;
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int e = (u * 32 + lane) * W;
-      if (write_bg) __stcs(reinterpret_cast<VT *>(dst + e), neg_inf_vec<T>());
-      else if (write_copy) __stcs(reinterpret_cast<VT *>(dst + e), v[u]);
+      for (int u = 0; u < U; ++u) st_cs_splat4(pd + u * 32, ni);
+    } else if (write_copy) {
+#pragma unroll
+      for (int u = 0; u < U; ++u) __stcs(pd + u * 32, v[u]);
     }
   } else {  // ragged tail chunk of the row: element-wise, same (u, lane, w) layout
     for (int u = 0; u < U; ++u) {
@@ -146,10 +154,11 @@ __device__ __forceinline__ void consume_chunk(const uint8_t *stage, int c0, int 
   base = __shfl_sync(0xffffffffu, base, 31);
   if (base >= (uint32_t)kCapXF + gcap) return;  // X is full: the outliers are only counted
   uint32_t pos = base + incl - cnt;
+  const int le = lane * W;  // element of bit j: (j / W) * 32 * W + lane * W + j % W
   while (m) {
     const int j = __ffsll((long long)m) - 1;
     m &= m - 1;
-    const int e = ((j / W) * 32 + lane) * W + (j % W);
+    const int e = ((j & ~(W - 1)) << 5) + le + (j & (W - 1));
     const uint32_t bits = Elem<T>::bits(st[e]);
     if (HIST) {
       const uint32_t bin = (key_of_bits(bits) - bl - 1u) >> bsh;
@@ -194,6 +203,12 @@ __global__ void __launch_bounds__(kFusedThreads, 2) qrita_fused(Params P) {
       const uint32_t bytes = (uint32_t)(min(CE, V - c * CE) * (int)sizeof(T));
       mbar_arrive_expect_tx(&fs.full[slot], bytes);
       tma_load_1d(ring + (size_t)slot * kStageBytes, in + (size_t)c * CE, bytes, &fs.full[slot], pol);
+#if QRITA_L2_PREFETCH
+      // the chunk kRing further on goes to L2 now: its ring load then waits for an L2 hit instead of a
+      // loaded HBM round trip, doubling the bytes in flight per CTA without shared memory
+      if (c + kRing < nch)
+        l2_prefetch_bulk(in + (size_t)(c + kRing) * CE, (uint32_t)(min(CE, V - (c + kRing) * CE) * (int)sizeof(T)));
+#endif
     };
     if (tid == 0) {  // fill the ring; afterwards each consumed stage is refilled by its consumer
       fence_proxy_async_smem();  // the previous row's tail wrote the ring through the generic proxy
@@ -225,8 +240,9 @@ __global__ void __launch_bounds__(kFusedThreads, 2) qrita_fused(Params P) {
       const bool hist = mode == MODE_TOPK || mode == MODE_TOPKP;
       const uint32_t bl = pl.key_thr - 1u;
       const int bsh = pl.bsh;
-      const bool write_bg = !inplace && (mode == MODE_TOPK || mode == MODE_TOPKP || mode == MODE_INVALID);
-      const bool write_copy = !inplace && mode == MODE_PASS;
+      const bool has_out = P.out != nullptr;  // index-only calls write no masked logits
+      const bool write_bg = has_out && !inplace && (mode == MODE_TOPK || mode == MODE_TOPKP || mode == MODE_INVALID);
+      const bool write_copy = has_out && !inplace && mode == MODE_PASS;
       T *dst = (T *)P.out + (size_t)row * P.ld_out;
       uint32_t *gxb = P.cand_bits + (size_t)row * P.xcap, *gxi = P.cand_idx + (size_t)row * P.xcap;
       // (2) stream: warp w consumes chunks w, w + 8, ...

@@ -419,6 +419,66 @@ __device__ void write_row(const T *in, T *out, int V, uint32_t K, uint32_t cut, 
   }
 }
 
+// Kept-column list of a row (index-only output, SURVEY.md 8b kept_idx): every column with
+// kept_by(key, i, K, cut) is appended to dst through a shared counter; order unspecified.  Warp-
+// converged loops (uniform trip counts) so the per-warp reservation can use full-mask shuffles.
+__device__ __forceinline__ uint32_t warp_reserve_n(uint32_t *ctr, uint32_t n) {
+  const int lane = threadIdx.x & 31;
+  uint32_t incl = n;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += t;
+  }
+  const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
+  uint32_t base = 0u;
+  if (lane == 0 && tot) base = atomicAdd(ctr, tot);
+  return __shfl_sync(0xffffffffu, base, 0) + incl - n;
+}
+
+template <typename T>
+__device__ void write_row_idx(const T *in, int V, uint32_t K, uint32_t cut, int32_t *dst, uint32_t *ctr) {
+  using VT = typename Vec<T>::type;
+  constexpr int W = Vec<T>::W;
+  const int tid = threadIdx.x;
+  if (((uintptr_t)in % 16) == 0 && V % W == 0) {
+    const VT *pi = reinterpret_cast<const VT *>(in);
+    const int nv = V / W;
+    const VecCmp<T> cmp(K);
+    for (int b0 = 0; b0 < nv; b0 += kThreads * kLd) {
+      VT r[kLd];
+#pragma unroll
+      for (int j = 0; j < kLd; ++j)
+        if (b0 + j * kThreads + tid < nv) r[j] = __ldcg(pi + b0 + j * kThreads + tid);
+#pragma unroll
+      for (int j = 0; j < kLd; ++j) {
+        const int vi = b0 + j * kThreads + tid;
+        uint32_t kp = 0u;
+        if (vi < nv) {
+          uint32_t gt, eq;
+          cmp.masks(r[j], gt, eq);
+          kp = gt;
+#pragma unroll
+          for (int w = 0; w < W; ++w)
+            if (((eq >> w) & 1u) && (uint32_t)(vi * W + w) <= cut) kp |= 1u << w;
+        }
+        uint32_t pos = warp_reserve_n(ctr, (uint32_t)__popc(kp));
+        while (kp) {
+          const int w = __ffs(kp) - 1;
+          kp &= kp - 1u;
+          dst[pos++] = vi * W + w;
+        }
+      }
+    }
+    return;
+  }
+  for (int i0 = 0; i0 < V; i0 += kThreads) {
+    const int i = i0 + tid;
+    const bool kp = i < V && kept_by(key_of_bits(Elem<T>::bits(in[i])), (uint32_t)i, K, cut);
+    const uint32_t pos = warp_reserve_n(ctr, kp ? 1u : 0u);
+    if (kp) dst[pos] = i;
+  }
+}
 
 // Row tail proper, run by the tail thread group (kThreads threads, tsync barriers) once the row's
 // outliers X = (xb, xi)[0, n_c) are in shared memory (in any order; only when they fit: n_c <= kCapX
@@ -476,6 +536,8 @@ __device__ void tail_resolve(const Params &P, int row, const RowPlan &pl, uint32
   const int mode = pl.mode;
   if (mode == MODE_INVALID) return;
   if (mode == MODE_PASS) {  // _passthrough, pipeline.py:81-85 (the stream already copied the row)
+    if (P.kept_idx)
+      for (int i = tid; i < V; i += kThreads) P.kept_idx[(size_t)row * P.ld_idx + i] = i;
     if (tid == 0) {
       met.kept_count = V;
       met.row_passes = 1;
@@ -878,10 +940,32 @@ __device__ void tail_resolve(const Params &P, int row, const RowPlan &pl, uint32
 
   QRITA_TSTAMP(8);
   // ================= output: finalize_mask, pipeline.py:60-78 =================
-  if (mode == MODE_TOPP || inplace || (!sorted_out && !k_used_x)) {
+  // kept-column list (kept_idx): the same four sources as the masked values below
+  if (P.kept_idx) {
+    int32_t *dst = P.kept_idx + (size_t)row * P.ld_idx;
+    if (tid == 0) sm.u[6] = 0u;
+    tsync();
+    if (mode == MODE_TOPP || (!sorted_out && !k_used_x)) {
+      if (!P.out && tid == 0) ++sm.row_passes;  // (with masked output, write_row's pass is counted below)
+      write_row_idx<T>(in, V, Kf, cutf, dst, &sm.u[6]);
+    } else if (sorted_out) {
+      for (int q = tid; q < (int)kept; q += kThreads) dst[q] = (int32_t)di[q];
+    } else {
+      for (int i0 = 0; i0 < X.n; i0 += kThreads) {
+        const int i = i0 + tid;
+        const bool kp = i < X.n && kept_by(key_of_bits(xb[i]), xi[i], Kf, cutf);
+        const uint32_t pos = warp_reserve_n(&sm.u[6], kp ? 1u : 0u);
+        if (kp) dst[pos] = (int32_t)xi[i];
+      }
+    }
+    tsync();
+  }
+  if (!P.out) {  // index-only call
+  } else if (mode == MODE_TOPP || inplace || (!sorted_out && !k_used_x)) {
     if (tid == 0) ++sm.row_passes;  // write_row reads the whole row again
   }
-  if (mode == MODE_TOPP) {
+  if (!P.out) {
+  } else if (mode == MODE_TOPP) {
     write_row<T>(in, out, V, Kf, cutf, inplace ? 2 : 1);  // the stream left top-p-only rows alone
   } else if (inplace) {
     write_row<T>(in, out, V, Kf, cutf, 2);

@@ -124,8 +124,9 @@ __global__ void __launch_bounds__(kStreamThreads, 3) qrita_stream(Params P) {
     const int mode = plp->mode;
     // outlier iff z >= thr (float compare: -0.0 == +0.0 as in the reference); NaN threshold = none
     const float thr = plp->has_thr ? __uint_as_float(bits_of_key(plp->key_thr)) : qnan;
-    const bool write_bg = !inplace && (mode == MODE_TOPK || mode == MODE_TOPKP || mode == MODE_INVALID);
-    const bool write_copy = !inplace && mode == MODE_PASS;
+    const bool has_out = P.out != nullptr;  // index-only calls write no masked logits
+    const bool write_bg = has_out && !inplace && (mode == MODE_TOPK || mode == MODE_TOPKP || mode == MODE_INVALID);
+    const bool write_copy = has_out && !inplace && mode == MODE_PASS;
     // finite identities, so lanes without elements (ragged chunks) never look non-finite
     float fmx = -3.402823466e38f, fmn = 3.402823466e38f;
     uint32_t base = 0u;

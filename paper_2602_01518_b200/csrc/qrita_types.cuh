@@ -95,6 +95,8 @@ struct Params {
   const double *p;
   int32_t *kept_count;
   qrita_row_metrics *metrics;
+  int32_t *kept_idx;        // [B][ld_idx] kept columns (unordered), or NULL; out may be NULL (index-only)
+  int64_t ld_idx;
   // workspace
   RowPlan *plans;
   RowAgg *agg;              // [B]

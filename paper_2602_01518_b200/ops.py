@@ -218,6 +218,65 @@ def topk_topp(logits: torch.Tensor, k: Union[int, torch.Tensor], p: Union[float,
     return out
 
 
+def topk_topp_indices(logits: torch.Tensor, k: Union[int, torch.Tensor], p: Union[float, torch.Tensor], *,
+                      kept_idx: Optional[torch.Tensor] = None, kept_count: Optional[torch.Tensor] = None,
+                      out: Optional[torch.Tensor] = None, flags: Optional[TruncFlags] = None,
+                      sample_size: int = DEFAULT_SAMPLE_SIZE, metrics: Optional[torch.Tensor] = None,
+                      check: bool = True, stream: Optional[torch.cuda.Stream] = None
+                      ) -> Tuple[torch.Tensor, torch.Tensor]:
+    """The kept columns of every row instead of (or besides, when `out` is given) the masked logits
+    (qrita_topk_topp_idx; SURVEY.md 8b kept_idx).  Same selection as topk_topp.  Returns (kept_idx
+    int32 [B, V], kept_count int32 [B]): row r's kept columns are kept_idx[r, :kept_count[r]], in
+    unspecified order.  Without `out` only V * sizeof(dtype) is read and kept * 4 bytes written per
+    row, about half of the masked-logit traffic.  CUDA tensors only; stream-ordered like topk_topp."""
+    if not isinstance(logits, torch.Tensor) or not logits.is_cuda:
+        raise TypeError("topk_topp_indices takes a CUDA tensor")
+    if logits.dim() != 2:
+        raise ValueError("logit batch must be 2-D (rows x vocab)")
+    if logits.dtype not in _DTYPES:
+        raise TypeError(f"unsupported dtype {logits.dtype}; expected float32 or bfloat16")
+    if logits.stride(1) != 1 or (logits.shape[0] > 1 and logits.stride(0) < logits.shape[1]):
+        logits = logits.contiguous()
+    b, v = logits.shape
+    if b == 0 or v == 0:
+        raise ValueError("batch_size and vocab_size must be >= 1")
+    if sample_size < 1:
+        raise ValueError("sample_size must be >= 1")
+    dev = logits.device
+    kt = _per_row(k, b, torch.int64, dev, "k")
+    pt = _per_row(p, b, torch.float64, dev, "p")
+    if kept_idx is None:
+        kept_idx = torch.empty((b, v), dtype=torch.int32, device=dev)
+    elif kept_idx.dtype != torch.int32 or kept_idx.dim() != 2 or kept_idx.shape[0] != b or \
+            kept_idx.shape[1] < v or kept_idx.stride(1) != 1:
+        raise ValueError("kept_idx must be int32 [B, >= V] with unit column stride")
+    if kept_count is None:
+        kept_count = torch.empty((b,), dtype=torch.int32, device=dev)
+    if out is not None and (out.shape != logits.shape or out.dtype != logits.dtype or out.stride(1) != 1):
+        raise ValueError("out must match logits in shape/dtype with unit column stride")
+    fl = (flags or TruncFlags()).bits()
+    st = stream or torch.cuda.current_stream(dev)
+    lib = N.load()
+    need = lib.qrita_workspace_bytes(b, v, _DTYPES[logits.dtype], fl)
+    ws = workspace_for(dev, st)
+    with torch.cuda.device(dev):
+        ws_ptr, ws_bytes = ws.get(need, st)
+        rc = lib.qrita_topk_topp_idx(
+            ctypes.c_void_p(logits.data_ptr()), _row_stride(logits), _DTYPES[logits.dtype], b, v,
+            ctypes.c_void_p(kt.data_ptr()), ctypes.c_void_p(pt.data_ptr()),
+            ctypes.c_void_p(out.data_ptr() if out is not None else 0), _row_stride(out) if out is not None else v,
+            ctypes.c_void_p(kept_idx.data_ptr()), kept_idx.stride(0),
+            ctypes.c_void_p(kept_count.data_ptr()),
+            ctypes.c_void_p(metrics.data_ptr() if metrics is not None else 0),
+            ctypes.c_void_p(ws_ptr), ws_bytes, fl, int(sample_size), ctypes.c_void_p(st.cuda_stream))
+        if rc != N.OK:
+            ws.reset()
+            raise RuntimeError(f"qrita_topk_topp_idx failed: {N.strerror(rc)}")
+        if check:
+            check_status(ws_ptr, b, logits, kt, pt, st)
+    return kept_idx, kept_count
+
+
 def pipeline_kind(logits: torch.Tensor, flags: Optional[TruncFlags] = None) -> str:
     """Which kernel pipeline qrita_topk_topp runs for this tensor (mirrors the dispatch in
     csrc/qrita_impl.cuh launch_all): "fused" (one launch: qrita_fused) when rows are 16-byte aligned

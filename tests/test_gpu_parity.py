@@ -371,3 +371,52 @@ def test_capi_host_numpy_binding(cuda_device):
                                     None, None, sp, nbytes - 1, rows, 0, 4096, st) == N.EWORKSPACE
     assert lib.qrita_topk_topp_host(xs.ctypes.data, 0, B, V, kk.ctypes.data, pp.ctypes.data, out.ctypes.data,
                                     None, None, sp, nbytes, 0, 0, 4096, st) == N.EINVAL_ARG
+
+
+def _idx_sets(kidx, kc):
+    return [np.sort(kidx[r, :kc[r]]) for r in range(kidx.shape[0])]
+
+
+@pytest.mark.parametrize("cfg", ["cfg2", "cfg3"])
+def test_kept_indices_configs(cuda_device, cfg):
+    """qrita_topk_topp_idx: index-only output (no masked logits) and indices beside the masked
+    logits, against the golden kept sets (bin-sort rows of cfg2, distinct-value rows of cfg3)."""
+    x, k, p, dtype, trip, _ = G.config(cfg)
+    n = 64
+    tdt = torch.bfloat16 if dtype == "bf16" else torch.float32
+    xt = torch.from_numpy(np.ascontiguousarray(x[:n])).cuda().to(tdt)
+    kt, pt = torch.from_numpy(k[:n]).cuda(), torch.from_numpy(p[:n]).cuda()
+    want = [np.nonzero(G.keep_from_trip(x[r], trip[r]))[0] for r in range(n)]
+    kidx, kc = Q.topk_topp_indices(xt, kt, pt)
+    got = _idx_sets(kidx.cpu().numpy(), kc.cpu().numpy())
+    for r in range(n):
+        assert np.array_equal(got[r], want[r]), f"{cfg} index-only row {r}"
+    out = torch.empty_like(xt)
+    kidx, kc = Q.topk_topp_indices(xt, kt, pt, out=out)
+    got = _idx_sets(kidx.cpu().numpy(), kc.cpu().numpy())
+    o = out.float().cpu().numpy()
+    for r in range(n):
+        assert np.array_equal(got[r], want[r]), f"{cfg} indices beside logits row {r}"
+        assert np.array_equal(np.nonzero(~np.isneginf(o[r]))[0], want[r])
+
+
+def test_kept_indices_paths(cuda_device):
+    """Every source of the kept list: pass-through rows, sorted candidates, X compaction (pivot
+    search over the outliers), full-row compaction (fallback / top-p only / staged / unaligned V),
+    fp32 and bf16, against the oracle."""
+    rng = np.random.default_rng(77)
+    for v in (4096, 5000, 40000):
+        x = rng.normal(size=(8, v)).astype(np.float32)
+        x[3] = np.round(x[3] * 3) / 3
+        k = np.array([v, 50, 2000, 7, v, 300, 1, v], np.int64)
+        p = np.array([1.0, 0.9, 0.8, 1.0, 0.95, 1.0, 0.5, 0.3])
+        for dtype in (torch.float32, torch.bfloat16):
+            xs = x if dtype == torch.float32 else (to_bf16_bits(x).astype(np.uint32) << 16).view(np.float32)
+            want = [np.nonzero(oracle_keep_row(xs[r], int(k[r]), float(p[r])))[0] for r in range(8)]
+            xt = torch.from_numpy(xs).cuda().to(dtype)
+            for fl in (None, Q.TruncFlags(force_fallback=True), Q.TruncFlags(search="binary"), Q.TruncFlags(use_sigma_trunc=False),
+                       Q.TruncFlags(staged=True)):
+                kidx, kc = Q.topk_topp_indices(xt, torch.from_numpy(k).cuda(), torch.from_numpy(p).cuda(), flags=fl)
+                got = _idx_sets(kidx.cpu().numpy(), kc.cpu().numpy())
+                for r in range(8):
+                    assert np.array_equal(got[r], want[r]), (v, dtype, fl, r, k[r], p[r])

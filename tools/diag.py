@@ -148,16 +148,18 @@ if len(sys.argv) > 1 and sys.argv[1] == "ftiming":
         xt = torch.from_numpy(x).cuda().to(tdt)
         kt, pt = torch.from_numpy(k).cuda(), torch.from_numpy(p).cuda()
         fl = Q.TruncFlags(debug_timing=True)
+        # IDX=1: index-only output (topk_topp_indices, no masked logits)
+        call = (lambda *a, **kw: Q.topk_topp_indices(*a, **kw)) if os.environ.get("IDX") else Q.topk_topp
         st = torch.cuda.current_stream()
         ws = Q.ops.workspace_for(xt.device, st)
         for _ in range(3):
-            Q.topk_topp(xt, kt, pt, flags=fl)
+            call(xt, kt, pt, flags=fl)
         ptr, _ = ws.get(0, st)
         B = x.shape[0]
         ws.buf.zero_()
         if os.environ.get("FLUSH"):  # evict the kernel's code and data from L2 first (serving-like)
             fl_buf = torch.empty(64 << 20, device="cuda"); fl_buf.zero_(); fl_buf.sum()
-        Q.topk_topp(xt, kt, pt, flags=fl)
+        call(xt, kt, pt, flags=fl)
         buf = (ctypes.c_ulonglong * (16 * B))()
         N.load().qrita_get_timing(ctypes.c_void_p(ptr), B, buf, ctypes.c_void_p(st.cuda_stream))
         a = np.frombuffer(buf, dtype=np.uint64).reshape(B, 16).astype(np.int64)
