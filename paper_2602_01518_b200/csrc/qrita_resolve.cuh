@@ -11,45 +11,6 @@
 
 namespace qrita {
 
-// Visits every element of a row in global memory, fn(i, valid, bits) with fp32-expanded bits, called by
-// all lanes (warp-converged, for match_any aggregation).  16-byte vector loads, kLd in flight per
-// thread, when the row is aligned.
-template <typename T, class Fn>
-__device__ __forceinline__ void for_row_warp(const T *in, int V, Fn fn) {
-  using VT = typename Vec<T>::type;
-  constexpr int W = Vec<T>::W;
-  const int tid = threadIdx.x;
-  if (((uintptr_t)in % 16) == 0 && V % W == 0) {
-    const VT *p = reinterpret_cast<const VT *>(in);
-    const int nv = V / W;
-    for (int b0 = 0; b0 < nv; b0 += kThreads * kLd) {
-      VT r[kLd];
-#pragma unroll
-      for (int j = 0; j < kLd; ++j) {
-        const int vi = b0 + j * kThreads + tid;
-        if (vi < nv) r[j] = __ldcg(p + vi);
-      }
-#pragma unroll
-      for (int j = 0; j < kLd; ++j) {
-        const int vi = b0 + j * kThreads + tid;
-#pragma unroll
-        for (int w = 0; w < W; ++w) fn(vi * W + w, vi < nv, vi < nv ? lane_bits<T>(r[j], w) : 0u);
-      }
-    }
-  } else {
-    for (int b0 = 0; b0 < V; b0 += kThreads * kLd) {
-      uint32_t r[kLd];
-#pragma unroll
-      for (int j = 0; j < kLd; ++j) {
-        const int i = b0 + j * kThreads + tid;
-        r[j] = i < V ? Elem<T>::bits(in[i]) : 0u;
-      }
-#pragma unroll
-      for (int j = 0; j < kLd; ++j) fn(b0 + j * kThreads + tid, b0 + j * kThreads + tid < V, r[j]);
-    }
-  }
-}
-
 struct DistinctRes {
   bool ok;        // false: too many distinct values, use the pivot search
   bool keep_all;  // p >= fsum(all)
@@ -60,8 +21,8 @@ struct DistinctRes {
 
 // Top-p over a whole row through its distinct values (pipeline.py:161-196 semantics of oracle.py:37-67).
 // Equal logits have equal probabilities, so the nucleus only needs each distinct value's count: one
-// pass counts them into a shared-memory hash table (warp-aggregated with match_any), then the
-// distinct values are sorted descending (bin counting sort) and fp64 exp, the exact normaliser
+// pass counts them into a shared-memory hash table (batched probes; one shared atomic per
+// element), then the distinct values are sorted descending (bin counting sort) and fp64 exp, the exact normaliser
 // D = sum count * exp(v - m), probabilities fl(e / D) and the exact prefix masses are computed per
 // distinct value.  Rows with few distinct values (bf16 / quantised logits) cost one row pass instead
 // of a pivot search with an fp64 exp per element per pass.  tk/tc: table of cap (power of two)
