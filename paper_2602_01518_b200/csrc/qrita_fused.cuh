@@ -35,6 +35,9 @@ namespace qrita {
 constexpr int kStageBytes = 4096;
 constexpr int kCapXF = 5632;
 constexpr int kRing = 15;
+#ifndef QRITA_STREAM_HIST  // count the outliers into key bins while streaming (else in the tail, from X)
+#define QRITA_STREAM_HIST 1
+#endif
 #ifndef QRITA_L2_PREFETCH
 #define QRITA_L2_PREFETCH 0  // measured neutral on cfg2 / cfg4 (tools/ab2.sh); kept as an option
 #endif
@@ -237,7 +240,7 @@ __global__ void __launch_bounds__(kFusedThreads, 2) qrita_fused(Params P) {
       const bool inplace = (P.flags & QRITA_INPLACE) != 0;
       const int mode = pl.mode;
       const float thr = pl.has_thr ? __uint_as_float(bits_of_key(pl.key_thr)) : __uint_as_float(0x7fffffffu);
-      const bool hist = mode == MODE_TOPK || mode == MODE_TOPKP;
+      const bool hist = QRITA_STREAM_HIST && (mode == MODE_TOPK || mode == MODE_TOPKP);
       const uint32_t bl = pl.key_thr - 1u;
       const int bsh = pl.bsh;
       const bool has_out = P.out != nullptr;  // index-only calls write no masked logits
@@ -281,7 +284,7 @@ __global__ void __launch_bounds__(kFusedThreads, 2) qrita_fused(Params P) {
       }
       // (3) resolve; every stage of this row has been consumed, so the ring is the work area
       tail_resolve<T, NP>(P, row, pl, xb, xi, ring, fs.tail, fs.n_x, false, maxkey, minkey, nf_col,
-                          (uint32_t)kCapXF, gxb, gxi, (uint32_t)P.xcap, fs.hist, pl.bsh,
+                          (uint32_t)kCapXF, gxb, gxi, (uint32_t)P.xcap, QRITA_STREAM_HIST ? fs.hist : nullptr, pl.bsh,
                           (size_t)kRing * kStageBytes);
     }
     g0 += (uint32_t)nch;
