@@ -88,3 +88,33 @@ def test_product_has_no_oracle_dependency():
             if f.endswith(".py"):
                 src = open(os.path.join(dirpath, f)).read()
                 assert not re.search(r"^\s*(import oracle|from oracle)", src, flags=re.M), f
+
+
+def test_idx_and_host_entry_points_validate_before_cuda(lib):
+    """qrita_topk_topp_idx / qrita_topk_topp_host / qrita_host_scratch_bytes: argument checks that
+    return before any CUDA call (safe without a GPU)."""
+    dummy = ctypes.c_void_p(256)
+    V = 1000
+    # neither masked output nor kept_idx
+    assert lib.qrita_topk_topp_idx(dummy, V, 0, 4, V, dummy, dummy, None, V, None, V, dummy, None,
+                                   dummy, 1 << 20, 0, 4096, None) == N.EINVAL_ARG
+    # kept_idx narrower than V, or without kept_count / metrics to say how many entries are valid
+    assert lib.qrita_topk_topp_idx(dummy, V, 0, 4, V, dummy, dummy, None, V, dummy, V - 1, dummy, None,
+                                   dummy, 1 << 20, 0, 4096, None) == N.EINVAL_ARG
+    assert lib.qrita_topk_topp_idx(dummy, V, 0, 4, V, dummy, dummy, None, V, dummy, V, None, None,
+                                   dummy, 1 << 20, 0, 4096, None) == N.EINVAL_ARG
+    # index-only output cannot be in place
+    assert lib.qrita_topk_topp_idx(dummy, V, 0, 4, V, dummy, dummy, None, V, dummy, V, dummy, None,
+                                   dummy, 1 << 20, N.INPLACE, 4096, None) == N.EINVAL_ARG
+    # host pipeline: scratch size grows with B, covers both staging copies, rejects bad shapes
+    s1 = lib.qrita_host_scratch_bytes(8, V, 0, 4)
+    s2 = lib.qrita_host_scratch_bytes(16, V, 0, 4)
+    assert s2 > s1 >= 2 * 8 * V * 4
+    assert lib.qrita_host_scratch_bytes(8, V, 1, 4) < s1  # bf16 staging is half the size
+    assert lib.qrita_host_scratch_bytes(0, V, 0, 4) == 0 and lib.qrita_host_scratch_bytes(8, V, 0, 0) == 0
+    assert lib.qrita_topk_topp_host(dummy, 0, 8, V, dummy, dummy, dummy, None, None, dummy, s1, 0, 0, 4096,
+                                    None) == N.EINVAL_ARG
+    assert lib.qrita_topk_topp_host(dummy, 0, 8, V, dummy, dummy, dummy, None, None, dummy, s1 - 1, 4, 0, 4096,
+                                    None) == N.EWORKSPACE
+    assert lib.qrita_topk_topp_host(dummy, 0, 8, V, dummy, dummy, dummy, None, None, dummy, s1, 4, N.INPLACE,
+                                    4096, None) == N.EINVAL_ARG
