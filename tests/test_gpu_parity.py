@@ -199,6 +199,15 @@ def test_outlier_spill_rows(cuda_device):
         want = np.where(keep, x[i], -np.inf).astype(np.float32)
         assert G.same_bits(out[i], want).all(), i
         assert kept[i] == keep.sum()
+    # kept-column lists of the same spill rows (index-only and beside the masked logits)
+    xt = torch.from_numpy(x).cuda()
+    kt = torch.tensor(ks, dtype=torch.int64, device="cuda")
+    pt = torch.tensor(ps, dtype=torch.float64, device="cuda")
+    for o in (None, torch.empty_like(xt)):
+        kidx, kc = Q.topk_topp_indices(xt, kt, pt, out=o)
+        got = _idx_sets(kidx.cpu().numpy(), kc.cpu().numpy())
+        for i in range(x.shape[0]):
+            assert np.array_equal(got[i], np.nonzero(oracle_keep_row(x[i], ks[i], ps[i]))[0]), i
     xb = to_bf16_bits(x[:2])
     xf = (xb.astype(np.uint32) << 16).view(np.float32)
     out, kept, _ = run(xf, ks[:2], ps[:2], dtype=torch.bfloat16)
