@@ -164,7 +164,9 @@ __device__ __forceinline__ void consume_chunk(const uint8_t *stage, int c0, int 
     const int e = ((j & ~(W - 1)) << 5) + le + (j & (W - 1));
     const uint32_t bits = Elem<T>::bits(st[e]);
     if (HIST) {
-      const uint32_t bin = (key_of_bits(bits) - bl - 1u) >> bsh;
+      // a positive threshold makes every outlier a positive float: its key is bits | 2^31
+      const uint32_t key = bl >= 0x80000000u ? (bits | 0x80000000u) : key_of_bits(bits);
+      const uint32_t bin = (key - bl - 1u) >> bsh;
       atomicAdd(&hist[bin < (uint32_t)kNB ? bin : (uint32_t)(kNB - 1)], 1u);
     }
     if (pos < (uint32_t)kCapXF) {
