@@ -7,18 +7,24 @@ fp32 rows, per-row k ~ U{1..1024}, p ~ U[0.5, 0.99] (same law an
 reference's synth_batch).  Inputs are resident in HBM; L2 (126 MB) is flushed between timed steps
 by writing a 256 MB buffer; every step is timed with CUDA events on the launching stream.
 
-N > 1 (torchrun, one process per GPU): rows shard by construction — each rank truncates its own
-256-row batch with no collective (weak scaling); the job time is the max over ranks.
+Multi-GPU (one process per GPU): under torchrun every rank reads RANK / WORLD_SIZE; without torchrun,
+``--gpus N`` (N > 1) re-launches itself under torch.distributed.run with N ranks (and fails loudly if
+fewer than N GPUs are visible).  Rows shard by contiguous blocks, no collective on the data path:
+  cfg2 — weak scaling: every rank truncates its own 256-row batch (per-GPU work fixed);
+  cfg4 — strong scaling: the one B=1024 x V=262144 batch is split into contiguous B/N row blocks
+         (paper_2602_01518_b200.sharded.rank_rows), the BASELINE's row-sharded config.
+The job time is the max over ranks of the event-timed steps (synchronised start: barrier + sync).
 
-Extra keys beside the driver contract: roofline (dominant kernel qrita_main vs measured HBM peak),
-cpu_baseline (the oracle port on the host cores), torch_sort_baseline (serving-stack torch.sort
-recipe on the same GPU), e2e (pinned host buffers through the public API, copies inside).
+Extra keys beside the driver contract: roofline (dominant kernel qrita_fused vs the measured HBM
+peak), cpu_baseline (the reference's own run_batch on the host cores, persistent process pool),
+torch_sort_baseline (serving-stack torch.sort recipe on the same GPU), e2e (pinned host buffers
+through the public API, copies inside), e2e_run_batch (the reference's entry point run_batch on
+numpy arrays, everything inside).
 """
 from __future__ import annotations
 
 import argparse
 import json
-import math
 import os
 import statistics
 import sys
@@ -34,37 +40,61 @@ METRIC = "rows/sec and HBM GB/s (% of roofline) for Top-k+Top-p at B=256, V=128k
 FALLBACK_HBM_GBS = 6650.0
 
 
-def workload(name: str, rank: int = 0):
-    """Synthetic inputs (float32 matrix, k, p, dtype label) — same laws/seeds as SURVEY.md §8d."""
-    if name == "cfg2":
+def _normal_rows(seed: int, rows: int, vocab: int, lo: int, hi: int, chunk: int = 64) -> np.ndarray:
+    """Rows [lo, hi) of default_rng(seed).normal(0, 1, (rows, vocab)).astype(f32), generated in row
+    chunks so a rank holds only its own block (the draws are sequential: same values as one call)."""
+    rng = np.random.default_rng(seed)
+    out = np.empty((hi - lo, vocab), dtype=np.float32)
+    r = 0
+    while r < hi:
+        n = min(chunk, hi - r)
+        blk = rng.normal(0.0, 1.0, (n, vocab))
+        a, b = max(r, lo), min(r + n, hi)
+        if b > a:
+            out[a - lo:b - lo] = blk[a - r:b - r]
+        r += n
+    return out
+
+
+def workload(name: str, rank: int = 0, world: int = 1):
+    """Synthetic inputs of this rank (float32 matrix, k, p, dtype label, description, global rows,
+    scaling) — same laws / seeds as SURVEY.md §8d."""
+    if name == "cfg2":  # weak scaling: every rank owns a full 256-row batch of its own
         x = np.random.default_rng(1 + 1000 * rank).normal(0.0, 1.0, (256, 128256)).astype(np.float32)
         r = np.random.default_rng(42 + rank)
         return x, r.integers(1, 1025, 256).astype(np.int64), r.uniform(0.5, 0.99, 256), "f32", \
-            "cfg2: Llama-3 V=128256, B=256 fp32, k~U{1..1024}, p~U[0.5,0.99]"
+            "cfg2: Llama-3 V=128256, B=256 fp32, k~U{1..1024}, p~U[0.5,0.99]", 256 * world, "weak"
     if name == "cfg2h":  # first 128 rows of cfg2 (one row tail per SM)
-        x, k, p, dt, _ = workload("cfg2")
-        return x[:128].copy(), k[:128].copy(), p[:128].copy(), dt, "cfg2 rows 0-127"
+        x, k, p, dt, *_ = workload("cfg2")
+        return x[:128].copy(), k[:128].copy(), p[:128].copy(), dt, "cfg2 rows 0-127", 128 * world, "weak"
     if name == "cfg2copy":  # streaming floor: same matrix, k = V and p = 1 (passthrough copy)
         x = np.random.default_rng(1).normal(0.0, 1.0, (256, 128256)).astype(np.float32)
-        return x, np.full(256, 128256, np.int64), np.full(256, 1.0), "f32", "cfg2 matrix, passthrough"
+        return x, np.full(256, 128256, np.int64), np.full(256, 1.0), "f32", "cfg2 matrix, passthrough", \
+            256 * world, "weak"
     if name == "cfg2k":  # top-k only
         x = np.random.default_rng(1).normal(0.0, 1.0, (256, 128256)).astype(np.float32)
         r = np.random.default_rng(42)
-        return x, r.integers(1, 1025, 256).astype(np.int64), np.full(256, 1.0), "f32", "cfg2 top-k only"
+        return x, r.integers(1, 1025, 256).astype(np.int64), np.full(256, 1.0), "f32", "cfg2 top-k only", \
+            256 * world, "weak"
     if name == "cfg1":
         x = np.random.default_rng(0).normal(0.0, 1.0, (1, 32000)).astype(np.float32)
-        return x, np.full(1, 50, np.int64), np.full(1, 0.9), "f32", "cfg1: V=32000, B=1 fp32, k=50, p=0.9"
+        return x, np.full(1, 50, np.int64), np.full(1, 0.9), "f32", "cfg1: V=32000, B=1 fp32, k=50, p=0.9", \
+            world, "weak"
     if name == "cfg3":
         x = np.random.default_rng(3).normal(0.0, 1.0, (64, 151936)).astype(np.float32)
         neg = x < 0
         x[neg] = np.round(4.0 * x[neg]) / 4.0
         return x, np.full(64, 151936, np.int64), np.full(64, 0.95), "bf16", \
-            "cfg3: Qwen2 V=151936, B=64 bf16 quantised tail, top-p 0.95"
-    if name == "cfg4":
-        x = np.random.default_rng(4).normal(0.0, 1.0, (1024, 262144)).astype(np.float32)
+            "cfg3: Qwen2 V=151936, B=64 bf16 quantised tail, top-p 0.95", 64 * world, "weak"
+    if name == "cfg4":  # strong scaling: contiguous B/N row blocks of the one 1024-row batch
+        from paper_2602_01518_b200.sharded import rank_rows
+        lo, hi = rank_rows(1024, rank, world)
+        x = _normal_rows(4, 1024, 262144, lo, hi)
         r = np.random.default_rng(44)
-        return x, r.integers(1, 1025, 1024).astype(np.int64), r.uniform(0.5, 0.99, 1024), "f32", \
-            "cfg4: Gemma V=262144, B=1024 fp32, k~U{1..1024}, p~U[0.5,0.99]"
+        k, p = r.integers(1, 1025, 1024).astype(np.int64), r.uniform(0.5, 0.99, 1024)
+        return x, k[lo:hi].copy(), p[lo:hi].copy(), "f32", \
+            f"cfg4: Gemma V=262144, B=1024 fp32, k~U{{1..1024}}, p~U[0.5,0.99]; rows {lo}-{hi - 1} of 1024 " \
+            f"on this rank", 1024, "strong"
     raise ValueError(name)
 
 
@@ -147,59 +177,79 @@ def cpu_model() -> str:
     return "unknown"
 
 
-def cpu_baseline_oracle(x, k, p, rows: int, procs: int):
-    """The oracle port (oracle/qrita_oracle.py) over `rows` rows in `procs` processes."""
-    import concurrent.futures as cf
-
-    from oracle.qrita_oracle import oracle_keep_row  # noqa: F401  (import check in the parent)
-    chunks = np.array_split(np.arange(rows), procs)
-    t0 = time.perf_counter()
-    with cf.ProcessPoolExecutor(max_workers=procs) as ex:
-        futs = [ex.submit(_oracle_rows, x[c], k[c], p[c]) for c in chunks if c.size]
-        for f in futs:
-            f.result()
-    wall = time.perf_counter() - t0
-    return rows / wall, wall
-
-
-def _oracle_rows(x, k, p):
-    from oracle.qrita_oracle import oracle_keep_row
-    return [int(oracle_keep_row(x[i], int(k[i]), float(p[i])).sum()) for i in range(x.shape[0])]
+def cpu_reference(x, k, p, procs: int, steps: int, warmup: int, kind: str = "run_batch"):
+    """The reference's own CPU path on the host cores: sigmatop.run_batch (or sort_select) over
+    contiguous row chunks in a persistent pool of `procs` processes (oracle/cpu_baseline.py; pool
+    start-up outside the timed steps).  Falls back to the oracle port when the reference is not
+    installed in baseline/_ref.  Returns (rows/s, per-step seconds, record)."""
+    from oracle.cpu_baseline import CpuPool, reference_available
+    ok, why = reference_available()
+    pool_kind = kind if ok else "port"
+    rows = np.arange(x.shape[0])
+    with CpuPool(x, k, p, procs, pool_kind) as pool:
+        for _ in range(warmup):
+            pool.run(rows)
+        walls = [pool.run(rows) for _ in range(steps)]
+        startup = pool.startup_s
+    med = statistics.median(walls)
+    what = {"run_batch": "sigmatop.run_batch (pkg/src/sigmatop/engine.py:82-113, EngineConfig(threads=1) "
+                         "per process)",
+            "sort_select": "sigmatop.engine.sort_select (engine.py:183-205, the sort-based definition)",
+            "port": "oracle/qrita_oracle.py (numpy restatement of oracle.py:70-89; reference not installed: "
+                    + str(why) + ")"}[pool_kind]
+    rec = {"value": x.shape[0] / med, "unit": "rows/s", "cores": procs,
+           "kind": "reference" if ok else "port", "cpu_model": cpu_model(), "host_cores": os.cpu_count(),
+           "sample": f"all {x.shape[0]} rows of the workload per step through {what}, contiguous row "
+                     f"chunks over {procs} persistent worker processes; median of {steps} steps after "
+                     f"{warmup} warm-up; pool start-up {startup:.2f}s excluded",
+           "step_s": walls}
+    return x.shape[0] / med, walls, rec
 
 
 def run_reference(args):
-    """--impl reference: the reference's algorithm on the host cores (oracle port, all cores)."""
+    """--impl reference: the reference's own CPU implementation (sigmatop.run_batch from baseline/_ref)
+    on all host cores, on the same workload as our arm.  Under torchrun only rank 0 runs."""
     rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
     if rank != 0:
         return
-    x, k, p, dtype, desc = workload(args.config)
+    x, k, p, dtype, desc, total_rows, scaling = workload(args.config, 0, 1)
+    if args.config == "cfg4":  # the whole 1024-row batch (the CPU path is not sharded over GPUs)
+        x, k, p, dtype, desc, total_rows, scaling = workload(args.config, 0, 1)
     procs = os.cpu_count() or 1
-    per_step = procs
-    for _ in range(args.warmup):
-        cpu_baseline_oracle(x[:per_step], k[:per_step], p[:per_step], per_step, procs)
-    total_rows, total_wall = 0, 0.0
-    for s in range(args.steps):
-        lo = (s * per_step) % x.shape[0]
-        idx = (np.arange(per_step) + lo) % x.shape[0]
-        _, wall = cpu_baseline_oracle(x[idx], k[idx], p[idx], per_step, procs)
-        total_rows += per_step
-        total_wall += wall
-    value = total_rows / total_wall
+    value, walls, rec = cpu_reference(x, k, p, procs, args.steps, min(args.warmup, 2))
+    rec["value"] = value
     line = {
         "metric": METRIC, "value": value, "unit": "rows/s", "impl": "reference",
-        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * total_wall / args.steps, "higher_is_better": True, "scaling": "weak",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * statistics.median(walls), "higher_is_better": True, "scaling": scaling,
         "vs_baseline": None, "dtype": dtype, "data": "synthetic",
-        "config": {"workload": desc, "batch": int(x.shape[0]), "vocab": int(x.shape[1]),
-                   "sample_rows_per_step": per_step},
-        "cpu_baseline": {"value": value, "unit": "rows/s", "cores": procs, "kind": "port",
-                         "cpu_model": cpu_model(), "host_cores": os.cpu_count(),
-                         "sample": f"{per_step} rows of {args.config} per step through "
-                                   "oracle/qrita_oracle.py (numpy restatement of oracle.py:70-89), "
-                                   f"{procs} processes"},
+        "config": {"workload": desc, "batch": int(x.shape[0]), "vocab": int(x.shape[1])},
+        "cpu_baseline": rec,
         "e2e": {"value": value, "unit": "rows/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def _spawn_ranks(args) -> int:
+    """bench.py --gpus N outside torchrun: re-launch under torch.distributed.run with N ranks."""
+    import socket
+    import subprocess
+
+    import torch
+    have = torch.cuda.device_count()
+    if have < args.gpus:
+        print(json.dumps({"error": f"--gpus {args.gpus} needs {args.gpus} visible GPUs, found {have}"}),
+              flush=True)
+        sys.stderr.write(f"bench.py: --gpus {args.gpus} needs {args.gpus} visible GPUs, found {have}\n")
+        return 2
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
 
 
 def main():
@@ -213,8 +263,12 @@ def main():
     ap.add_argument("--no-extras", action="store_true", help="skip e2e / torch.sort / cpu legs")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
+    if args.gpus < 1:
+        ap.error("--gpus must be >= 1")
     if args.impl == "reference":
         return run_reference(args)
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        sys.exit(_spawn_ranks(args))
 
     import torch
     import torch.distributed as dist
@@ -225,14 +279,20 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        sys.stderr.write(f"bench.py: WORLD_SIZE={world} but --gpus {args.gpus}\n")
+        sys.exit(2)
     if world > 1:
+        if torch.cuda.device_count() <= local:
+            sys.stderr.write(f"bench.py: rank {rank} needs GPU {local}, {torch.cuda.device_count()} visible\n")
+            sys.exit(2)
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
 
-    x_np, k_np, p_np, dtype, desc = workload(args.config, rank)
+    x_np, k_np, p_np, dtype, desc, total_rows, scaling = workload(args.config, rank, world)
     tdt = torch.bfloat16 if dtype == "bf16" else torch.float32
     x = torch.from_numpy(x_np).to(dev).to(tdt)
     k = torch.from_numpy(k_np).to(dev)
@@ -263,7 +323,7 @@ def main():
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize(dev)
-    with ClockSampler(dev.index if world == 1 else local) as clk:
+    with ClockSampler(local) as clk:
         for i in range(args.steps):
             l2_flush()  # L2 flush between timed steps (not timed)
             step(*evs[i])
@@ -276,7 +336,7 @@ def main():
         t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
-    value = world * b * args.steps / (total_ms / 1e3)
+    value = total_rows * args.steps / (total_ms / 1e3)   # rows of ALL ranks / max-over-ranks time
     ms_per_step = total_ms / args.steps
 
     # per-kernel times (profiling iterations, untimed above): the events serialise the launches, so
@@ -298,13 +358,19 @@ def main():
     alg_bytes = b * v * esize * 2
     achieved = alg_bytes / (stream_ms / 1e3) / 1e9
     peak, peak_kind = measured_peak()
+    traffic = ncu_traffic(args.config)
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": achieved / peak, "traffic": ncu_traffic(args.config),
+                "frac": achieved / peak, "traffic": traffic,
                 "peak_source": peak_kind,
                 "kernel": "qrita_fused" if kind == "fused" else "qrita_stream",
                 "kernel_ms": stream_ms, "alg_bytes_per_launch": alg_bytes,
                 "alg_bytes_note": "B*V*sizeof(dtype) read + the same written (SURVEY.md 8d)",
                 "step_frac": alg_bytes / (ms_per_step / 1e3) / 1e9 / peak}
+    if traffic:
+        # DRAM-side rate: bytes ncu saw move during the kernel / its time (write-back of output still
+        # dirty in L2 at kernel end happens afterwards and is not in `traffic`)
+        roofline["dram_side_gbs"] = traffic / (stream_ms / 1e3) / 1e9
+        roofline["dram_side_frac"] = roofline["dram_side_gbs"] / peak
     if kind == "staged":
         roofline.update({"prep_ms": prep_ms, "tail_ms_serialised": tail_ms})
     launches_per_step = 1 if kind == "fused" else 3
@@ -316,10 +382,13 @@ def main():
     line = {
         "metric": METRIC, "value": value, "unit": "rows/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": dtype, "data": "synthetic",
-        "config": {"workload": desc, "batch": b, "vocab": v, "rows_per_gpu": b,
+        "scaling": scaling, "vs_baseline": None, "dtype": dtype, "data": "synthetic",
+        "config": {"workload": desc if world == 1 else desc.replace(" on this rank", " on rank 0"),
+                   "batch": total_rows, "vocab": v, "rows_per_gpu": b,
                    "l2": "flushed between steps (256 MB write + read-back, untimed)",
-                   "parallelism": f"row-sharded replicas x{world}, no collective"},
+                   "parallelism": f"row-sharded x{world} ({scaling} scaling: "
+                                  + ("each rank its own batch" if scaling == "weak" else "contiguous B/N row blocks")
+                                  + "), no collective"},
         "hbm_gbs": alg_bytes / (ms_per_step / 1e3) / 1e9,
         "roofline": roofline,
         "clocks": clk.summary(),
@@ -344,7 +413,7 @@ def main():
         sort_val = b / (statistics.mean(ts) / 1e3)
         line["torch_sort_baseline"] = {"value": sort_val, "unit": "rows/s",
                                        "ms_per_step": statistics.mean(ts), "exact": False,
-                                       "ours_over_sort": value / world / sort_val}
+                                       "ours_over_sort": (b / (ms_per_step / 1e3)) / sort_val}
         # index-only output (qrita_topk_topp_idx, out = NULL): kept columns instead of masked logits,
         # same selection; algorithmic bytes V*s read + kept*4 written per row
         kidx = torch.empty((b, v), dtype=torch.int32, device=dev)
@@ -383,28 +452,50 @@ def main():
                 tt.append(e0.elapsed_time(e1))
         h2d = x_host.numel() * x_host.element_size() + b * 16
         d2h = o_host.numel() * o_host.element_size() + b * 8  # masked logits + status words
-        e2e_val = b / (statistics.mean(tt) / 1e3)
-        if world > 1:
-            t = torch.tensor([statistics.mean(tt)], dtype=torch.float64, device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            e2e_val = world * b / (float(t.item()) / 1e3)
-        line["e2e"] = {"value": e2e_val, "unit": "rows/s", "h2d_bytes_per_step": h2d,
-                       "d2h_bytes_per_step": d2h, "ms_per_step": statistics.mean(tt),
+        e2e_ms = sharded_max(statistics.mean(tt), world, dev)
+        line["e2e"] = {"value": total_rows / (e2e_ms / 1e3), "unit": "rows/s", "h2d_bytes_per_step": h2d,
+                       "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms,
                        "api": "paper_2602_01518_b200.topk_topp(pinned host tensors)"}
+        # e2e through the reference's own entry point: run_batch(LogitBatch(numpy), TruncTargets(numpy))
+        # -> numpy float32 outputs + BatchReport (pageable host memory, validation, metrics report);
+        # host wall clock around the call (it returns with the result in host memory)
+        if dtype == "f32":
+            batch = Q.LogitBatch(x_np)
+            targets = Q.TruncTargets(k_np, p_np)
+            cfg = Q.EngineConfig()
+            rb = []
+            for i in range(e2e_steps + 2):
+                t0 = time.perf_counter()
+                outs, rep = Q.run_batch(batch, targets, cfg)
+                if i >= 2:
+                    rb.append(time.perf_counter() - t0)
+            rb_ms = sharded_max(1e3 * statistics.mean(rb), world, dev)
+            line["e2e_run_batch"] = {"value": total_rows / (rb_ms / 1e3), "unit": "rows/s", "ms_per_step": rb_ms,
+                                     "h2d_bytes_per_step": x_np.nbytes + b * 16,
+                                     "d2h_bytes_per_step": x_np.nbytes + b * 48,
+                                     "api": "paper_2602_01518_b200.run_batch(LogitBatch(numpy), TruncTargets(numpy), "
+                                            "EngineConfig()) -> (numpy outputs, BatchReport)"}
         if rank == 0 and world == 1 and not args.no_cpu_baseline:
-            rows = b
-            procs = min(os.cpu_count() or 1, rows)
-            val, wall = cpu_baseline_oracle(x_np, k_np, p_np, rows, procs)
-            line["cpu_baseline"] = {"value": val, "unit": "rows/s", "cores": procs, "kind": "port",
-                                    "cpu_model": cpu_model(), "host_cores": os.cpu_count(),
-                                    "sample": f"first {rows} rows of {args.config} through "
-                                              "oracle/qrita_oracle.py (numpy restatement of "
-                                              f"oracle.py:70-89), {procs} processes, {wall:.2f}s"}
+            procs = os.cpu_count() or 1
+            x_cpu = x.float().cpu().numpy() if dtype == "bf16" else x_np  # the values the GPU sees
+            val, walls, rec = cpu_reference(x_cpu, k_np, p_np, procs, steps=2, warmup=1)
+            line["cpu_baseline"] = rec
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
     if rank == 0:
         print(json.dumps(line), flush=True)
+
+
+def sharded_max(ms: float, world: int, dev) -> float:
+    """Max over ranks of a per-rank time (the job time)."""
+    if world == 1:
+        return ms
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
 
 
 if __name__ == "__main__":

@@ -298,18 +298,20 @@ constexpr size_t kFusedDynSmem = (size_t)kCapXF * 8 + (size_t)kRing * kStageByte
 
 template <typename T, int NP>
 static cudaError_t launch_fused(const Params &P, cudaStream_t st) {
-  static int grid_cap = 0;  // per instantiation
-  if (grid_cap == 0) {
+  static int grid_caps[kMaxDevices] = {};  // per instantiation and device
+  int grid_cap = 0;
+  cudaError_t e = per_device_once(grid_caps, [](int dev, int &cap) {
     cudaError_t e = cudaFuncSetAttribute(qrita_fused<T, NP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)kFusedDynSmem);
     if (e != cudaSuccess) return e;
-    int dev = 0, sms = 0, per_sm = 0;
-    cudaGetDevice(&dev);
+    int sms = 0, per_sm = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, qrita_fused<T, NP>, kFusedThreads, kFusedDynSmem);
     if (e != cudaSuccess) return e;
-    grid_cap = sms * (per_sm < 1 ? 1 : per_sm);
-  }
+    cap = sms * (per_sm < 1 ? 1 : per_sm);
+    return cudaSuccess;
+  }, grid_cap);
+  if (e != cudaSuccess) return e;
   // Balanced persistent grid: every CTA gets the same number of rows (no partial last wave), as
   // long as that keeps >= 3/4 of the CTA slots (and their ring bytes in flight) busy.
   int grid = P.B < grid_cap ? P.B : grid_cap;

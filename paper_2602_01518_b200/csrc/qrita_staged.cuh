@@ -230,13 +230,13 @@ constexpr size_t kTailDynSmem = (size_t)kCapX * 8 + (size_t)kWorkBytes;
 template <typename T, int NP, bool VEC>
 static cudaError_t launch_pipeline(const Params &P, cudaStream_t st, cudaEvent_t prep_done,
                                    cudaEvent_t stream_done) {
-  static int stream_grid = 0;  // per instantiation
-  if (stream_grid == 0) {
+  static int stream_grids[kMaxDevices] = {};  // per instantiation and device
+  int stream_grid = 0;
+  cudaError_t e0 = per_device_once(stream_grids, [](int dev, int &grid) {
     cudaError_t e = cudaFuncSetAttribute(qrita_tail<T, NP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)kTailDynSmem);
     if (e != cudaSuccess) return e;
-    int dev = 0, sms = 0, per_sm = 0;
-    cudaGetDevice(&dev);
+    int sms = 0, per_sm = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, qrita_stream<T, VEC>, kStreamThreads, 0);
     if (e != cudaSuccess) return e;
@@ -244,8 +244,10 @@ static cudaError_t launch_pipeline(const Params &P, cudaStream_t st, cudaEvent_t
     int want = 3;
     if (const char *ev = getenv("QRITA_STREAM_CTAS_PER_SM")) want = atoi(ev);
     if (want < 1) want = 1;
-    stream_grid = sms * (per_sm < want ? (per_sm < 1 ? 1 : per_sm) : want);
-  }
+    grid = sms * (per_sm < want ? (per_sm < 1 ? 1 : per_sm) : want);
+    return cudaSuccess;
+  }, stream_grid);
+  if (e0 != cudaSuccess) return e0;
   const Params &PP = P;
   qrita_prep<T><<<P.B, 256, 0, st>>>(PP);
   cudaError_t e = cudaGetLastError();

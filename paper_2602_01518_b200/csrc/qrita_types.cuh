@@ -120,6 +120,27 @@ struct WsLayout {
 
 inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
+// One-time launch setup per device: the dynamic shared-memory opt-in (cudaFuncSetAttribute) and the
+// occupancy-derived grid size belong to a device context, so they are cached per device ordinal.
+// `slots[dev]` holds the cached value (0 = not yet set up); concurrent first calls may both run
+// `init` (it is idempotent), and the value is published with release / acquire ordering.
+constexpr int kMaxDevices = 64;
+template <typename F>
+inline cudaError_t per_device_once(int *slots, F &&init, int &out) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (dev < 0 || dev >= kMaxDevices) return cudaErrorInvalidDevice;
+  int v = __atomic_load_n(&slots[dev], __ATOMIC_ACQUIRE);
+  if (v == 0) {
+    e = init(dev, v);
+    if (e != cudaSuccess) return e;
+    __atomic_store_n(&slots[dev], v, __ATOMIC_RELEASE);
+  }
+  out = v;
+  return cudaSuccess;
+}
+
 // Outlier buffer entries per row: a row never has more outliers than columns.
 inline __host__ __device__ int row_cap(int V) { return V < kCapX ? V : kCapX; }
 

@@ -84,7 +84,7 @@ def _device_inputs(batch: LogitBatch, targets: TruncTargets, device=None):
         else torch.device("cuda", torch.cuda.current_device()))
     x = batch.values
     if not _is_tensor(x):
-        x = torch.from_numpy(np.ascontiguousarray(x)).pin_memory().to(dev, non_blocking=True)
+        x = torch.from_numpy(np.ascontiguousarray(x)).to(dev)
     elif not x.is_cuda:
         x = x.to(dev)
     k = targets.k if _is_tensor(targets.k) else torch.from_numpy(np.ascontiguousarray(targets.k))
@@ -92,35 +92,86 @@ def _device_inputs(batch: LogitBatch, targets: TruncTargets, device=None):
     return x, k.to(dev, torch.int64), p.to(dev, torch.float64)
 
 
+_METRICS_DTYPE = np.dtype([("trunc_hit", "<i4"), ("outlier_count", "<i4"), ("outlier_prob_sum", "<f8"),
+                           ("k_search_iters", "<i4"), ("p_search_iters", "<i4"), ("fallback_used", "<i4"),
+                           ("kept_count", "<i4"), ("full_row_path", "<i4"), ("row_passes", "<i4")])
+assert _METRICS_DTYPE.itemsize == 40  # qrita_row_metrics (include/qrita_b200.h)
+
+
 def metrics_to_rows(buf: torch.Tensor) -> List[RowMetrics]:
-    rows = []
-    for m in ops.decode_metrics(buf):
-        rows.append(RowMetrics(trunc_hit=bool(m["trunc_hit"]), outlier_count=int(m["outlier_count"]),
-                               outlier_prob_sum=float(m["outlier_prob_sum"]),
-                               k_search_iters=int(m["k_search_iters"]),
-                               p_search_iters=int(m["p_search_iters"]),
-                               fallback_used=bool(m["fallback_used"])))
-    return rows
+    m = np.frombuffer(buf.cpu().numpy().tobytes(), dtype=_METRICS_DTYPE)
+    return [RowMetrics(trunc_hit=bool(h), outlier_count=int(c), outlier_prob_sum=float(s),
+                       k_search_iters=int(ik), p_search_iters=int(ip), fallback_used=bool(f))
+            for h, c, s, ik, ip, f in zip(m["trunc_hit"].tolist(), m["outlier_count"].tolist(),
+                                          m["outlier_prob_sum"].tolist(), m["k_search_iters"].tolist(),
+                                          m["p_search_iters"].tolist(), m["fallback_used"].tolist())]
 
 
-def run_batch(batch: LogitBatch, targets: TruncTargets, config: EngineConfig):
+def _host_targets_ok(batch: LogitBatch, targets: TruncTargets) -> bool:
+    """The O(B) part of validate_batch (lengths, k in [1, V], p in (0, 1]), vectorised; the O(B*V)
+    finiteness check runs on the device, fused into the truncation kernel (status block)."""
+    k = targets.k.cpu().numpy() if _is_tensor(targets.k) else np.asarray(targets.k)
+    p = targets.p.cpu().numpy() if _is_tensor(targets.p) else np.asarray(targets.p)
+    b, v = batch.batch_size, batch.vocab_size
+    return (k.shape == (b,) and p.shape == (b,) and bool(np.all((k >= 1) & (k <= v)))
+            and bool(np.all((p > 0.0) & (p <= 1.0))))
+
+
+def run_batch(batch: LogitBatch, targets: TruncTargets, config: EngineConfig, *, devices=None):
     """Truncate every row (engine.py:82-113).  Returns (outputs, BatchReport).
 
-    numpy input -> numpy float32 output (the reference's contract); CUDA tensor input -> CUDA
-    tensor output in the input dtype.
+    numpy input -> numpy float32 output (the reference's contract), through the library's native
+    host-buffer pipeline (qrita_topk_topp_host: row chunks copied in, truncated and copied back with
+    both PCIe directions overlapped with the kernels); CUDA tensor input -> CUDA tensor output in the
+    input dtype, one stream-ordered launch.  Invalid input raises the reference's
+    ValueError("invalid batch: ...") with the reference's report lines; logit finiteness is checked
+    on the device (fused into the kernel), k / p on the host.  devices=[...] shards the rows over
+    several GPUs in contiguous blocks (sharded.topk_topp_sharded).
     """
     if not isinstance(batch, LogitBatch):
         batch = LogitBatch(batch)
-    _check_inputs(batch, targets)
-    x, k, p = _device_inputs(batch, targets)
+    if not _host_targets_ok(batch, targets):
+        _check_inputs(batch, targets)      # the reference's full report (raises)
     b = batch.batch_size
-    met = ops.metrics_buffer(b, x.device)
-    torch.cuda.synchronize(x.device)
-    start = time.perf_counter_ns()
-    out = ops.topk_topp(x, k, p, flags=config.flags(), sample_size=config.sample_size,
-                        metrics=met, check=False)
-    torch.cuda.synchronize(x.device)
-    wall = time.perf_counter_ns() - start
+    on_gpu = _is_tensor(batch.values) and batch.values.is_cuda
+    if devices is not None and len(devices) > 1:
+        dev = torch.device("cuda", torch.cuda.current_device()) if not on_gpu else batch.values.device
+    elif devices is not None:
+        dev = torch.device(devices[0]) if not isinstance(devices[0], int) else torch.device("cuda", devices[0])
+    else:
+        dev = batch.values.device if on_gpu else torch.device("cuda", torch.cuda.current_device())
+    try:
+        if on_gpu:
+            x, k, p = _device_inputs(batch, targets, dev)
+            met = ops.metrics_buffer(b, x.device)
+            torch.cuda.synchronize(x.device)
+            start = time.perf_counter_ns()
+            if devices is not None and len(devices) > 1:
+                out = _sharded(x, k, p, config, devices, met)
+            else:
+                out = ops.topk_topp(x, k, p, flags=config.flags(), sample_size=config.sample_size,
+                                    metrics=met, check=True)
+            torch.cuda.synchronize(x.device)
+            wall = time.perf_counter_ns() - start
+        else:
+            vals = batch.values
+            xh = vals if _is_tensor(vals) else torch.from_numpy(np.ascontiguousarray(vals))
+            kh = targets.k.cpu() if _is_tensor(targets.k) else torch.from_numpy(np.asarray(targets.k, np.int64))
+            ph = targets.p.cpu() if _is_tensor(targets.p) else torch.from_numpy(np.asarray(targets.p, np.float64))
+            res = np.empty((b, batch.vocab_size), dtype=np.float32) if not _is_tensor(vals) else None
+            oh = torch.from_numpy(res) if res is not None else torch.empty_like(xh)
+            met = ops.metrics_buffer(b, dev)
+            start = time.perf_counter_ns()
+            if devices is not None and len(devices) > 1:
+                out = _sharded(xh, kh, ph, config, devices, met, out=oh)
+            else:
+                out = ops.topk_topp_host(xh, kh, ph, out=oh, flags=config.flags(), sample_size=config.sample_size,
+                                         metrics=met, check=True, device=dev)
+            wall = time.perf_counter_ns() - start
+            out = res if res is not None else out
+    except ops.TruncationError:
+        _check_inputs(batch, targets)      # the reference's exact report lines (raises)
+        raise
     per_row = metrics_to_rows(met)
     report = BatchReport(
         per_row=per_row,
@@ -131,9 +182,15 @@ def run_batch(batch: LogitBatch, targets: TruncTargets, config: EngineConfig):
         mean_iters_p=sum(m.p_search_iters for m in per_row) / b,
         wall_time_ns=wall,
         rows_per_second=b / (wall / 1e9) if wall > 0 else float("inf"))
-    if not _is_tensor(batch.values):
-        out = out.cpu().numpy()
     return out, report
+
+
+def _sharded(x, k, p, config: EngineConfig, devices, met: torch.Tensor, out=None):
+    """run_batch over several devices: per-block metrics are gathered into `met` (on its device)."""
+    from .sharded import topk_topp_sharded
+    res = topk_topp_sharded(x, k, p, devices, out=out, flags=config.flags(), sample_size=config.sample_size,
+                            check=True, metrics=met)
+    return res
 
 
 def verify_batch(batch: LogitBatch, targets: TruncTargets, config: EngineConfig,

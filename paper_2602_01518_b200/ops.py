@@ -145,19 +145,24 @@ def topk_topp(logits: torch.Tensor, k: Union[int, torch.Tensor], p: Union[float,
               out: Optional[torch.Tensor] = None, inplace: bool = False,
               flags: Optional[TruncFlags] = None, sample_size: int = DEFAULT_SAMPLE_SIZE,
               kept_count: Optional[torch.Tensor] = None, metrics: Optional[torch.Tensor] = None,
-              check: bool = True, stream: Optional[torch.cuda.Stream] = None,
+              check: Optional[bool] = None, stream: Optional[torch.cuda.Stream] = None,
               prep_event: Optional[torch.cuda.Event] = None,
               stream_event: Optional[torch.cuda.Event] = None) -> torch.Tensor:
     """Exact Top-k then Top-p truncation of a [B, V] tensor (fp32 or bf16) on the GPU.
 
-    CUDA tensors are truncated in place on their device (stream-ordered).  Host tensors go through
-    topk_topp_host: row chunks are copied in, truncated and copied back with the transfers of both
-    directions overlapped with the kernels (the result is a host tensor).
+    CUDA tensors are processed on their device, stream-ordered on `stream` (default: the current
+    stream); the masked logits go to a new tensor, to `out`, or — with inplace=True — back into
+    `logits` (which must then be row-contiguous: a tensor that would need a copy is rejected).  Host
+    tensors go through topk_topp_host: row chunks are copied in, truncated and copied back with the
+    transfers of both directions overlapped with the kernels (the result is a host tensor).
 
-    k: int64 per row (k == V disables top-k); p: float64 per row (p == 1 disables top-p).  Returns
-    the masked logits (new tensor, or `logits` itself when inplace).  kept_count (int32 [B]) and
-    metrics (uint8 [B, 40], qrita_row_metrics) are filled when given.  check=True synchronises and
-    raises the reference's ValueError for invalid rows; check=False leaves the call fully async.
+    k: int64 per row (k == V disables top-k); p: float64 per row (p == 1 disables top-p).  kept_count
+    (int32 [B]) and metrics (uint8 [B, 40], qrita_row_metrics) are filled when given.
+
+    check: raise the reference's ValueError for invalid rows (non-finite logits, k outside [1, V], p
+    outside (0, 1]).  Checking SYNCHRONISES the stream and reads the device status block, so the
+    default is check=False for CUDA tensors (the call stays fully asynchronous; invalid rows get
+    undefined output) and check=True for host tensors (that call synchronises anyway).
     prep_event / stream_event (profiling only) are recorded after the preparation / streaming kernel;
     either one serialises the launches around it so the kernels can be timed alone.
     """
@@ -165,14 +170,18 @@ def topk_topp(logits: torch.Tensor, k: Union[int, torch.Tensor], p: Union[float,
         if inplace or prep_event is not None or stream_event is not None:
             raise ValueError("host tensors support neither inplace nor profiling events")
         return topk_topp_host(logits, k, p, out=out, flags=flags, sample_size=sample_size,
-                              kept_count=kept_count, metrics=metrics, check=check)
+                              kept_count=kept_count, metrics=metrics, check=True if check is None else check)
     if not isinstance(logits, torch.Tensor):
         raise TypeError("logits must be a torch tensor")
     if logits.dim() != 2:
         raise ValueError("logit batch must be 2-D (rows x vocab)")
     if logits.dtype not in _DTYPES:
         raise TypeError(f"unsupported dtype {logits.dtype}; expected float32 or bfloat16")
+    if check is None:
+        check = False
     if logits.stride(1) != 1 or (logits.shape[0] > 1 and logits.stride(0) < logits.shape[1]):
+        if inplace:
+            raise ValueError("inplace=True needs rows with unit column stride (this tensor would be copied)")
         logits = logits.contiguous()
     b, v = logits.shape
     if b == 0 or v == 0:
@@ -180,20 +189,23 @@ def topk_topp(logits: torch.Tensor, k: Union[int, torch.Tensor], p: Union[float,
     if sample_size < 1:
         raise ValueError("sample_size must be >= 1")
     dev = logits.device
-    kt = _per_row(k, b, torch.int64, dev, "k")
-    pt = _per_row(p, b, torch.float64, dev, "p")
-    if inplace:
-        out = logits
-    elif out is None:
-        out = torch.empty_like(logits)
-    elif out.shape != logits.shape or out.dtype != logits.dtype or out.stride(1) != 1:
+    st = stream or torch.cuda.current_stream(dev)
+    if out is not None and not inplace and (out.shape != logits.shape or out.dtype != logits.dtype or
+                                            out.stride(1) != 1):
         raise ValueError("out must match logits in shape/dtype with unit column stride")
     fl = (flags or TruncFlags()).bits() | (N.INPLACE if inplace else 0)
-    st = stream or torch.cuda.current_stream(dev)
     lib = N.load()
     need = lib.qrita_workspace_bytes(b, v, _DTYPES[logits.dtype], fl)
     ws = workspace_for(dev, st)
-    with torch.cuda.device(dev):
+    # temporaries (k / p in the kernel's dtypes, the output, the workspace) are created on the
+    # launching stream, so the kernel never races their initialisation or their reuse
+    with torch.cuda.device(dev), torch.cuda.stream(st):
+        kt = _per_row(k, b, torch.int64, dev, "k")
+        pt = _per_row(p, b, torch.float64, dev, "p")
+        if inplace:
+            out = logits
+        elif out is None:
+            out = torch.empty_like(logits)
         ws_ptr, ws_bytes = ws.get(need, st)
         ev = ev2 = 0
         if prep_event is not None:
@@ -222,13 +234,14 @@ def topk_topp_indices(logits: torch.Tensor, k: Union[int, torch.Tensor], p: Unio
                       kept_idx: Optional[torch.Tensor] = None, kept_count: Optional[torch.Tensor] = None,
                       out: Optional[torch.Tensor] = None, flags: Optional[TruncFlags] = None,
                       sample_size: int = DEFAULT_SAMPLE_SIZE, metrics: Optional[torch.Tensor] = None,
-                      check: bool = True, stream: Optional[torch.cuda.Stream] = None
+                      check: Optional[bool] = None, stream: Optional[torch.cuda.Stream] = None
                       ) -> Tuple[torch.Tensor, torch.Tensor]:
     """The kept columns of every row instead of (or besides, when `out` is given) the masked logits
     (qrita_topk_topp_idx; SURVEY.md 8b kept_idx).  Same selection as topk_topp.  Returns (kept_idx
     int32 [B, V], kept_count int32 [B]): row r's kept columns are kept_idx[r, :kept_count[r]], in
     unspecified order.  Without `out` only V * sizeof(dtype) is read and kept * 4 bytes written per
-    row, about half of the masked-logit traffic.  CUDA tensors only; stream-ordered like topk_topp."""
+    row, about half of the masked-logit traffic.  CUDA tensors only; stream-ordered like topk_topp
+    (check defaults to False: pass check=True to synchronise and raise for invalid rows)."""
     if not isinstance(logits, torch.Tensor) or not logits.is_cuda:
         raise TypeError("topk_topp_indices takes a CUDA tensor")
     if logits.dim() != 2:
@@ -243,15 +256,11 @@ def topk_topp_indices(logits: torch.Tensor, k: Union[int, torch.Tensor], p: Unio
     if sample_size < 1:
         raise ValueError("sample_size must be >= 1")
     dev = logits.device
-    kt = _per_row(k, b, torch.int64, dev, "k")
-    pt = _per_row(p, b, torch.float64, dev, "p")
-    if kept_idx is None:
-        kept_idx = torch.empty((b, v), dtype=torch.int32, device=dev)
-    elif kept_idx.dtype != torch.int32 or kept_idx.dim() != 2 or kept_idx.shape[0] != b or \
-            kept_idx.shape[1] < v or kept_idx.stride(1) != 1:
+    if check is None:
+        check = False
+    if kept_idx is not None and (kept_idx.dtype != torch.int32 or kept_idx.dim() != 2 or
+                                 kept_idx.shape[0] != b or kept_idx.shape[1] < v or kept_idx.stride(1) != 1):
         raise ValueError("kept_idx must be int32 [B, >= V] with unit column stride")
-    if kept_count is None:
-        kept_count = torch.empty((b,), dtype=torch.int32, device=dev)
     if out is not None and (out.shape != logits.shape or out.dtype != logits.dtype or out.stride(1) != 1):
         raise ValueError("out must match logits in shape/dtype with unit column stride")
     fl = (flags or TruncFlags()).bits()
@@ -259,7 +268,13 @@ def topk_topp_indices(logits: torch.Tensor, k: Union[int, torch.Tensor], p: Unio
     lib = N.load()
     need = lib.qrita_workspace_bytes(b, v, _DTYPES[logits.dtype], fl)
     ws = workspace_for(dev, st)
-    with torch.cuda.device(dev):
+    with torch.cuda.device(dev), torch.cuda.stream(st):
+        kt = _per_row(k, b, torch.int64, dev, "k")
+        pt = _per_row(p, b, torch.float64, dev, "p")
+        if kept_idx is None:
+            kept_idx = torch.empty((b, v), dtype=torch.int32, device=dev)
+        if kept_count is None:
+            kept_count = torch.empty((b,), dtype=torch.int32, device=dev)
         ws_ptr, ws_bytes = ws.get(need, st)
         rc = lib.qrita_topk_topp_idx(
             ctypes.c_void_p(logits.data_ptr()), _row_stride(logits), _DTYPES[logits.dtype], b, v,
@@ -312,20 +327,36 @@ _host_scratch = {}
 DEFAULT_HOST_CHUNK_BYTES = 16 << 20  # measured best on cfg2 (tools/e2e_sweep.py)
 
 
-def _scratch_for(device: torch.device, nbytes: int) -> torch.Tensor:
-    """Per-device device scratch of the host-buffer pipeline, grown on demand (256-byte aligned)."""
+def _scratch_for(device: torch.device, nbytes: int, slot: int = 0) -> torch.Tensor:
+    """Device scratch of the host-buffer pipeline per (device, slot), grown on demand (256-byte
+    aligned).  Concurrent host-buffer calls on one device (topk_topp_sharded with a repeated device)
+    use different slots."""
     with _host_lock:
-        buf = _host_scratch.get(device.index)
+        buf = _host_scratch.get((device.index, slot))
         if buf is None or buf.numel() < nbytes + 256:
             buf = torch.empty(nbytes + 256, dtype=torch.uint8, device=device)
-            _host_scratch[device.index] = buf
+            _host_scratch[(device.index, slot)] = buf
         return buf
+
+
+_side_streams = {}
+
+
+def side_stream(device: torch.device, slot: int) -> torch.cuda.Stream:
+    """A library-owned CUDA stream per (device, slot) (row blocks of topk_topp_sharded)."""
+    with _host_lock:
+        st = _side_streams.get((device.index, slot))
+        if st is None:
+            st = torch.cuda.Stream(device=device)
+            _side_streams[(device.index, slot)] = st
+        return st
 
 
 def topk_topp_host(logits: torch.Tensor, k, p, *, out: Optional[torch.Tensor] = None,
                    flags: Optional[TruncFlags] = None, sample_size: int = DEFAULT_SAMPLE_SIZE,
                    kept_count: Optional[torch.Tensor] = None, metrics: Optional[torch.Tensor] = None,
-                   check: bool = True, device=None, chunk_bytes: int = DEFAULT_HOST_CHUNK_BYTES) -> torch.Tensor:
+                   check: bool = True, device=None, chunk_bytes: int = DEFAULT_HOST_CHUNK_BYTES,
+                   scratch_slot: int = 0) -> torch.Tensor:
     """topk_topp for a host [B, V] tensor through qrita_topk_topp_host: the library copies row chunks
     of ~chunk_bytes in, truncates each as soon as it has landed and copies it back, on three streams
     of its own, so both PCIe directions stay busy and overlap the kernels.  Pinned host memory gives
@@ -361,7 +392,7 @@ def topk_topp_host(logits: torch.Tensor, k, p, *, out: Optional[torch.Tensor] = 
     need = lib.qrita_host_scratch_bytes(b, v, dt, rows)
     with torch.cuda.device(dev):
         st = torch.cuda.current_stream(dev)
-        buf = _scratch_for(dev, need)
+        buf = _scratch_for(dev, need, scratch_slot)
         base = buf.data_ptr()
         sp = (base + 255) & ~255
         rc = lib.qrita_topk_topp_host(

@@ -19,7 +19,7 @@ def run(x, k, p, dtype=torch.float32, **flags):
     kept = torch.zeros(xt.shape[0], dtype=torch.int32, device="cuda")
     met = Q.ops.metrics_buffer(xt.shape[0], xt.device)
     out = Q.topk_topp(xt, kt, pt, flags=Q.TruncFlags(**flags) if flags else None, kept_count=kept,
-                      metrics=met)
+                      metrics=met, check=True)
     torch.cuda.synchronize()
     return out.float().cpu().numpy(), kept.cpu().numpy(), Q.ops.decode_metrics(met)
 
@@ -158,9 +158,9 @@ def test_device_side_nonfinite_status(cuda_device):
     x = torch.randn(3, 5000, device="cuda")
     x[1, 1234] = float("nan")
     with pytest.raises(ValueError, match="NaN logit at row 1, col 1234"):
-        Q.topk_topp(x, 10, 0.9)
+        Q.topk_topp(x, 10, 0.9, check=True)
     with pytest.raises(ValueError, match="k out of range"):
-        Q.topk_topp(torch.randn(2, 100, device="cuda"), torch.tensor([5, 101], device="cuda"), 0.5)
+        Q.topk_topp(torch.randn(2, 100, device="cuda"), torch.tensor([5, 101], device="cuda"), 0.5, check=True)
 
 
 def test_pipeline_row_api(cuda_device):
@@ -338,7 +338,7 @@ def test_mixed_modes_many_rows_per_cta(cuda_device):
         assert G.same_bits(got[i], want).all(), (i, k[i], p[i])
         assert kc[i] == keep.sum(), i
     with pytest.raises(ValueError, match="non-finite logit at row 303, col 4321"):
-        Q.topk_topp(xt, torch.from_numpy(k).cuda(), torch.from_numpy(p).cuda())
+        Q.topk_topp(xt, torch.from_numpy(k).cuda(), torch.from_numpy(p).cuda(), check=True)
 
 
 def test_row_passes_metric(cuda_device):
