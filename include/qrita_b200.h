@@ -136,8 +136,10 @@ int qrita_topk_topp_ex(const void *logits, int64_t ld_in, int dtype, int B, int 
 
 /*
  * Host-buffer variant (the reference's run_batch takes host arrays, engine.py:82-113): logits / out
- * are HOST [B, V] row-major arrays (page-locked memory lets the copies run asynchronously), k / p are
- * HOST arrays.  Row chunks of `chunk_rows` rows are copied in, truncated and copied back on three
+ * are HOST [B, V] row-major arrays, k / p are HOST arrays.  Page-locked buffers are copied by DMA
+ * directly; pageable buffers are staged through two library-owned page-locked slots per direction,
+ * filled / drained by a pool of host threads (QRITA_HOST_COPY_THREADS) one chunk ahead of / behind
+ * the DMA — with a pageable `out_host` the call returns only once the result is in it.  Row chunks of `chunk_rows` rows are copied in, truncated and copied back on three
  * streams owned by the library (upload / truncate / download), ordered by per-chunk events, so both
  * PCIe directions and the kernels overlap.  `scratch` is a DEVICE buffer of
  * qrita_host_scratch_bytes(B, V, dtype, chunk_rows) bytes, 256-byte aligned (no initialisation

@@ -6,7 +6,10 @@
 #include <string.h>
 
 #include <algorithm>
+#include <atomic>
+#include <condition_variable>
 #include <mutex>
+#include <thread>
 #include <vector>
 
 #include "qrita_types.cuh"
@@ -105,10 +108,14 @@ HostLayout host_layout(int B, int V, int dtype, int chunk_rows) {
 }
 
 // The library's own streams and a growing event pool, per device; one host-buffer call enqueues at a
-// time (the events are reused across calls, so the enqueue section is serialised).
+// time (the events are reused across calls, so the enqueue section is serialised).  Pageable host
+// buffers are staged through two page-locked slots per direction (grown on demand).
 struct HostPipe {
   cudaStream_t up = nullptr, comp = nullptr, down = nullptr;
   std::vector<cudaEvent_t> ev;
+  void *stage_in[2] = {nullptr, nullptr}, *stage_out[2] = {nullptr, nullptr};
+  size_t stage_bytes = 0;
+  cudaEvent_t in_free[2] = {nullptr, nullptr}, out_ready[2] = {nullptr, nullptr};
 };
 std::mutex g_host_mu;
 HostPipe g_host_pipe[64];
@@ -124,7 +131,111 @@ cudaError_t host_pipe_get(int dev, size_t nev, HostPipe *&hp) {
     if ((e = cudaEventCreateWithFlags(&x, cudaEventDisableTiming)) != cudaSuccess) return e;
     hp->ev.push_back(x);
   }
+  for (int i = 0; i < 2; ++i)
+    for (cudaEvent_t *x : {&hp->in_free[i], &hp->out_ready[i]})
+      if (!*x && (e = cudaEventCreateWithFlags(x, cudaEventDisableTiming)) != cudaSuccess) return e;
   return cudaSuccess;
+}
+
+cudaError_t host_stage_reserve(HostPipe *hp, size_t bytes) {
+  if (hp->stage_bytes >= bytes) return cudaSuccess;
+  for (int i = 0; i < 2; ++i) {
+    // the slots may still feed copies of the previous call
+    if (hp->in_free[i]) cudaEventSynchronize(hp->in_free[i]);
+    if (hp->out_ready[i]) cudaEventSynchronize(hp->out_ready[i]);
+    for (void **b : {&hp->stage_in[i], &hp->stage_out[i]}) {
+      if (*b) cudaFreeHost(*b);
+      *b = nullptr;
+    }
+  }
+  hp->stage_bytes = 0;
+  for (int i = 0; i < 2; ++i)
+    for (void **b : {&hp->stage_in[i], &hp->stage_out[i]}) {
+      cudaError_t e = cudaHostAlloc(b, bytes, cudaHostAllocPortable);
+      if (e != cudaSuccess) return e;
+    }
+  hp->stage_bytes = bytes;
+  return cudaSuccess;
+}
+
+// Parallel host memcpy for the pageable staging copies: a persistent pool of worker threads (the
+// calling thread helps); one copy at a time.  QRITA_HOST_COPY_THREADS overrides the thread count.
+class CopyPool {
+ public:
+  static CopyPool &get() {
+    static CopyPool *pool = new CopyPool();  // never destroyed: its threads end with the process
+    return *pool;
+  }
+  void copy(void *d, const void *s, size_t n) {
+    if (n < (1u << 20) || nthreads_ == 0) {
+      memcpy(d, s, n);
+      return;
+    }
+    std::lock_guard<std::mutex> call(call_mu_);
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      dst_ = (uint8_t *)d;
+      src_ = (const uint8_t *)s;
+      bytes_ = n;
+      size_t piece = n / (size_t)(4 * (nthreads_ + 1));
+      piece = std::max<size_t>(piece, 256u << 10);
+      piece_ = (piece + 4095) & ~(size_t)4095;
+      next_.store(0);
+      active_ = nthreads_;
+      ++gen_;
+    }
+    cv_work_.notify_all();
+    run_pieces();
+    std::unique_lock<std::mutex> lk(mu_);
+    cv_done_.wait(lk, [&] { return active_ == 0; });
+  }
+
+ private:
+  CopyPool() {
+    // half the hardware threads, at most 8: measured best on the 16-core B200 host (cfg2 run_batch
+    // 5.0 ms with 8 copiers vs 6.5 ms with 16, tools/e2e_pageable.py)
+    int n = std::min(8, std::max(1, (int)std::thread::hardware_concurrency() / 2));
+    if (const char *ev = getenv("QRITA_HOST_COPY_THREADS")) n = atoi(ev);
+    n = std::max(0, std::min(n, 32) - 1);  // the caller is one of the copiers
+    nthreads_ = n;
+    for (int i = 0; i < n; ++i) std::thread([this] { worker(); }).detach();
+  }
+  void run_pieces() {
+    for (;;) {
+      const size_t off = next_.fetch_add(1) * piece_;
+      if (off >= bytes_) return;
+      memcpy(dst_ + off, src_ + off, std::min(piece_, bytes_ - off));
+    }
+  }
+  void worker() {
+    uint64_t seen = 0;
+    std::unique_lock<std::mutex> lk(mu_);
+    for (;;) {
+      cv_work_.wait(lk, [&] { return gen_ != seen; });
+      seen = gen_;
+      lk.unlock();
+      run_pieces();
+      lk.lock();
+      if (--active_ == 0) cv_done_.notify_all();
+    }
+  }
+  std::mutex call_mu_, mu_;
+  std::condition_variable cv_work_, cv_done_;
+  int nthreads_ = 0, active_ = 0;
+  uint64_t gen_ = 0;
+  uint8_t *dst_ = nullptr;
+  const uint8_t *src_ = nullptr;
+  size_t bytes_ = 0, piece_ = 0;
+  std::atomic<size_t> next_{0};
+};
+
+bool is_pinned(const void *p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
 }
 
 }  // namespace
@@ -304,16 +415,42 @@ int qrita_topk_topp_host(const void *logits_host, int dtype, int B, int V,
   if (!ok(cudaMemcpyAsync(sc + H.k, k_host, 8ull * (size_t)B, cudaMemcpyHostToDevice, hp->up)) ||
       !ok(cudaMemcpyAsync(sc + H.p, p_host, 8ull * (size_t)B, cudaMemcpyHostToDevice, hp->up)))
     return QRITA_ECUDA;
-  for (size_t c = 0; c < nc; ++c) {
+  // Page-locked host buffers: every upload is enqueued up front, then the kernels and downloads.
+  // Pageable buffers: the host copies each chunk into a page-locked slot (CopyPool, many threads)
+  // right before its upload, and each downloaded chunk out of its slot one chunk later, so the DMA
+  // of chunk c overlaps the host copies of chunks c +- 1.
+  const bool in_staged = !is_pinned(logits_host), out_staged = !is_pinned(out_host);
+  if ((in_staged || out_staged) &&
+      host_stage_reserve(hp, (size_t)H.chunks[0].second * row_bytes) != cudaSuccess)
+    return QRITA_ECUDA;
+  auto upload = [&](size_t c) -> bool {
     const size_t r0 = (size_t)H.chunks[c].first, nr = (size_t)H.chunks[c].second;
-    if (!ok(cudaMemcpyAsync(sc + H.in + r0 * row_bytes, (const uint8_t *)logits_host + r0 * row_bytes,
-                            nr * row_bytes, cudaMemcpyHostToDevice, hp->up)) ||
+    const uint8_t *src = (const uint8_t *)logits_host + r0 * row_bytes;
+    if (in_staged) {
+      const int slot = (int)(c & 1);
+      if (!ok(cudaEventSynchronize(hp->in_free[slot]))) return false;  // its previous upload is done
+      CopyPool::get().copy(hp->stage_in[slot], src, nr * row_bytes);
+      src = (const uint8_t *)hp->stage_in[slot];
+    }
+    if (!ok(cudaMemcpyAsync(sc + H.in + r0 * row_bytes, src, nr * row_bytes, cudaMemcpyHostToDevice, hp->up)) ||
         !ok(cudaEventRecord(landed[c], hp->up)))
-      return QRITA_ECUDA;
+      return false;
+    if (in_staged && !ok(cudaEventRecord(hp->in_free[c & 1], hp->up))) return false;
     if (trace) cudaEventRecord(tr[c], hp->up);
-  }
+    return true;
+  };
+  auto drain = [&](size_t c) -> bool {  // staged output: chunk c from its slot to the caller's buffer
+    const size_t r0 = (size_t)H.chunks[c].first, nr = (size_t)H.chunks[c].second;
+    if (!ok(cudaEventSynchronize(hp->out_ready[c & 1]))) return false;
+    CopyPool::get().copy((uint8_t *)out_host + r0 * row_bytes, hp->stage_out[c & 1], nr * row_bytes);
+    return true;
+  };
+  if (!in_staged)
+    for (size_t c = 0; c < nc; ++c)
+      if (!upload(c)) return QRITA_ECUDA;
   for (size_t c = 0; c < nc; ++c) {
     const size_t r0 = (size_t)H.chunks[c].first, nr = (size_t)H.chunks[c].second;
+    if (in_staged && !upload(c)) return QRITA_ECUDA;
     if (!ok(cudaStreamWaitEvent(hp->comp, landed[c], 0))) return QRITA_ECUDA;
     const int rc = topk_topp_impl(sc + H.in + r0 * row_bytes, V, dtype, (int)nr, V,
                                   (const int64_t *)(sc + H.k) + r0, (const double *)(sc + H.p) + r0,
@@ -323,12 +460,21 @@ int qrita_topk_topp_host(const void *logits_host, int dtype, int B, int V,
                                   (int32_t *)(sc + H.nf) + r0);
     if (rc != QRITA_OK) return rc;
     if (trace) cudaEventRecord(tr[nc + c], hp->comp);
-    if (!ok(cudaEventRecord(done[c], hp->comp)) || !ok(cudaStreamWaitEvent(hp->down, done[c], 0)) ||
-        !ok(cudaMemcpyAsync((uint8_t *)out_host + r0 * row_bytes, sc + H.out + r0 * row_bytes, nr * row_bytes,
-                            cudaMemcpyDeviceToHost, hp->down)))
+    if (!ok(cudaEventRecord(done[c], hp->comp)) || !ok(cudaStreamWaitEvent(hp->down, done[c], 0)))
       return QRITA_ECUDA;
+    if (out_staged) {
+      if (!ok(cudaMemcpyAsync(hp->stage_out[c & 1], sc + H.out + r0 * row_bytes, nr * row_bytes,
+                              cudaMemcpyDeviceToHost, hp->down)) ||
+          !ok(cudaEventRecord(hp->out_ready[c & 1], hp->down)))
+        return QRITA_ECUDA;
+      if (c > 0 && !drain(c - 1)) return QRITA_ECUDA;
+    } else if (!ok(cudaMemcpyAsync((uint8_t *)out_host + r0 * row_bytes, sc + H.out + r0 * row_bytes,
+                                   nr * row_bytes, cudaMemcpyDeviceToHost, hp->down))) {
+      return QRITA_ECUDA;
+    }
     if (trace) cudaEventRecord(tr[2 * nc + c], hp->down);
   }
+  if (out_staged && !drain(nc - 1)) return QRITA_ECUDA;
   if (trace) {
     cudaDeviceSynchronize();
     for (size_t c = 0; c < nc; ++c) {

@@ -158,8 +158,11 @@ def run_batch(batch: LogitBatch, targets: TruncTargets, config: EngineConfig, *,
             xh = vals if _is_tensor(vals) else torch.from_numpy(np.ascontiguousarray(vals))
             kh = targets.k.cpu() if _is_tensor(targets.k) else torch.from_numpy(np.asarray(targets.k, np.int64))
             ph = targets.p.cpu() if _is_tensor(targets.p) else torch.from_numpy(np.asarray(targets.p, np.float64))
-            res = np.empty((b, batch.vocab_size), dtype=np.float32) if not _is_tensor(vals) else None
-            oh = torch.from_numpy(res) if res is not None else torch.empty_like(xh)
+            # the numpy result lives in page-locked memory from torch's caching host allocator (the array
+            # keeps the block alive): downloads go straight into it, and no fresh pages are faulted in
+            oh = torch.empty((b, batch.vocab_size), dtype=torch.float32, pin_memory=True) \
+                if not _is_tensor(vals) else torch.empty_like(xh, pin_memory=True)
+            res = oh.numpy() if not _is_tensor(vals) else None
             met = ops.metrics_buffer(b, dev)
             start = time.perf_counter_ns()
             if devices is not None and len(devices) > 1:
