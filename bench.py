@@ -292,6 +292,8 @@ def main():
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
 
+    if args.config == "cfg5":
+        return bench_tp(args, rank, world, dev)
     x_np, k_np, p_np, dtype, desc, total_rows, scaling = workload(args.config, rank, world)
     tdt = torch.bfloat16 if dtype == "bf16" else torch.float32
     x = torch.from_numpy(x_np).to(dev).to(tdt)
@@ -480,6 +482,75 @@ def main():
             x_cpu = x.float().cpu().numpy() if dtype == "bf16" else x_np  # the values the GPU sees
             val, walls, rec = cpu_reference(x_cpu, k_np, p_np, procs, steps=2, warmup=1)
             line["cpu_baseline"] = rec
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
+def bench_tp(args, rank: int, world: int, dev):
+    """cfg5: vocab-sharded (TP = world) truncation of B=128 x V=262144 fp32, every rank its column
+    shard; per-row partials through a library-owned NCCL communicator (qrita_topk_topp_tp).  Job time
+    = max over ranks of the event-timed calls."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2602_01518_b200.tp import NcclComm, shard_bounds, topk_topp_tp
+    b, v = 128, 262144
+    x_np = np.random.default_rng(5).normal(0.0, 1.0, (b, v)).astype(np.float32)
+    r = np.random.default_rng(55)
+    k_np, p_np = r.integers(1, 1025, b).astype(np.int64), r.uniform(0.5, 0.99, b)
+    bounds = shard_bounds(v, world)
+    shard = torch.from_numpy(x_np[:, bounds[rank]:bounds[rank + 1]].copy()).to(dev)
+    k, p = torch.from_numpy(k_np).to(dev), torch.from_numpy(p_np).to(dev)
+    out = torch.empty_like(shard)
+    comm = NcclComm()
+    kcap = int(k_np.max())
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    st = torch.cuda.current_stream(dev)
+
+    def call():
+        topk_topp_tp(shard, k, p, vocab_offset=bounds[rank], vocab_size=v, comm=comm, k_cap=kcap, out=out,
+                     topp_only_rows=False)
+    for _ in range(args.warmup):
+        flush.zero_()
+        call()
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(args.steps)]
+    with ClockSampler(dev.index) as clk:
+        for e0, e1 in evs:
+            flush.zero_()
+            if world > 1:
+                dist.barrier()   # synchronised start of every step
+            e0.record(st)
+            call()
+            e1.record(st)
+        torch.cuda.synchronize(dev)
+    ms = statistics.mean(a.elapsed_time(c) for a, c in evs)
+    ms = sharded_max(ms, world, dev)
+    peak, peak_kind = measured_peak()
+    alg = b * (bounds[rank + 1] - bounds[rank]) * 4 * 2
+    kmax = min(kcap, bounds[rank + 1] - bounds[rank])
+    line = {
+        "metric": METRIC, "value": b / (ms / 1e3), "unit": "rows/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": f"cfg5: vocab-sharded TP={world}, B=128 x V=262144 fp32, k~U{{1..1024}}, "
+                               f"p~U[0.5,0.99]; shard [128, {bounds[1] - bounds[0]}] per rank",
+                   "batch": b, "vocab": v, "l2": "flushed between steps",
+                   "parallelism": f"tp{world} (vocab shards, NCCL partials)"},
+        "roofline": {"bound": "hbm", "achieved": alg / (ms / 1e3) / 1e9, "peak": peak, "unit": "GB/s",
+                     "frac": alg / (ms / 1e3) / 1e9 / peak, "traffic": None, "peak_source": peak_kind,
+                     "kernel": "whole qrita_topk_topp_tp call (kernels + collectives)",
+                     "alg_bytes_per_launch": alg},
+        "exchange_bytes_per_row_per_rank": 8 * kmax + 4,
+        "clocks": clk.summary(),
+        "gpu_launches": 6 * args.steps,
+    }
+    comm.close()
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()

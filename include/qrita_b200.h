@@ -54,8 +54,10 @@ enum {
   QRITA_INPLACE         = 1 << 4, /* out == logits (pipeline.py:72-74)                               */
   QRITA_RESERVED_5      = 1 << 5, /* reserved (rejected)                                            */
   QRITA_DEBUG_TIMING    = 1 << 6, /* record per-row tail phase timestamps (qrita_get_timing)        */
-  QRITA_STAGED          = 1 << 7  /* force the staged 3-kernel pipeline (prep / stream / tail) even
+  QRITA_STAGED          = 1 << 7, /* force the staged 3-kernel pipeline (prep / stream / tail) even
                                      when the fused single-kernel path applies                      */
+  QRITA_TP_NO_TOPP_ROWS = 1 << 8  /* vocab-sharded call only: the caller guarantees no row is top-p
+                                     only (k == V_global, p < 1), so the top-p rounds are skipped   */
 };
 
 /* return codes */
@@ -67,7 +69,7 @@ enum {
   QRITA_ENONFINITE = 4,   /* some logit is NaN or +-inf                     */
   QRITA_EWORKSPACE = 5,   /* workspace too small / misaligned              */
   QRITA_ECUDA = 6,        /* a CUDA runtime call failed                     */
-  QRITA_ENCCL = 7         /* reserved for the vocab-sharded variant         */
+  QRITA_ENCCL = 7         /* a collective of the vocab-sharded variant failed */
 };
 
 /* Per-row accounting, field-for-field the reference RowMetrics (core.py:72-81) plus kept_count
@@ -156,6 +158,66 @@ int qrita_topk_topp_host(const void *logits_host, int dtype, int B, int V,
 /* qrita_get_status for the last qrita_topk_topp_host call on `scratch` (same B, V, chunk_rows). */
 int qrita_get_status_host(const void *scratch, int B, int V, int dtype, int chunk_rows, int *row, int *col,
                           qrita_stream_t stream);
+
+/*
+ * Vocab-sharded (tensor-parallel LM-head) variant — BASELINE cfg5, SURVEY.md 8(b)/8(e).
+ *
+ * Every rank holds the columns [vocab_offset, vocab_offset + V_shard) of the [B, V_global] logits
+ * (shards contiguous, offsets increasing with rank) and receives its shard of the UNSHARDED answer,
+ * bit-exact.  Only per-row partials cross ranks (include: what is exchanged, bytes per row):
+ *   1. local top-min(k, V_shard) candidates (top-p-only rows: the local max), one all-gather of
+ *      (order key, global column) pairs, sorted by column: <= 8 * k_cap bytes per row per rank;
+ *      every rank resolves top-k + top-p on the gathered candidates with the single-GPU kernels
+ *      (global stable order, full-row max and survivor normaliser all live in that set);
+ *   2. top-p-only rows only: the exact normaliser (fixed-point limbs, integer all-reduce SUM: exact
+ *      and order-independent), then 4 (bf16) / 8 (fp32) radix passes, each an all-reduce SUM of 16
+ *      (count, exact mass) partials per row, then one all-reduce of the per-rank boundary-tie counts
+ *      (ties are kept in global index order, i.e. rank order).
+ *
+ *   logits / out   device [B, ld_in] / [B, ld_out] shard (out may equal logits with QRITA_INPLACE)
+ *   k, p           device int64 / float64 [B], the GLOBAL targets (k == V_global disables top-k)
+ *   k_cap          >= every k < V_global in the batch (rows violating it report QRITA_EINVAL_ARG
+ *                  through qrita_get_status); bounds the candidate exchange
+ *   kept_count     device int32 [B] or NULL: entries kept in THIS shard
+ *   flags          0, QRITA_INPLACE, QRITA_TP_NO_TOPP_ROWS
+ *   workspace      qrita_tp_workspace_bytes(...) bytes, zeroed before first use (qrita_workspace_init)
+ * Status (non-finite logits of this shard, bad k / p) is read with qrita_get_status(workspace, B).
+ */
+typedef struct qrita_comm {
+  /* in-place all-reduce SUM of `count` unsigned integers of `elem_bytes` (4 or 8) bytes each in the
+   * DEVICE buffer `buf`, ordered on `stream`; returns 0 on success */
+  int (*all_reduce_sum)(void *buf, size_t count, int elem_bytes, qrita_stream_t stream, void *ctx);
+  /* all-gather: DEVICE `send` (bytes_per_rank bytes) of every rank into DEVICE `recv`
+   * (world * bytes_per_rank, rank order), ordered on `stream`; returns 0 on success */
+  int (*all_gather)(const void *send, void *recv, size_t bytes_per_rank, qrita_stream_t stream, void *ctx);
+  void *ctx;
+} qrita_comm;
+
+size_t qrita_tp_workspace_bytes(int B, int V_shard, int dtype, int world, int k_cap);
+
+int qrita_topk_topp_tp_comm(const void *logits, int64_t ld_in, int dtype, int B, int V_shard,
+                            int V_global, int64_t vocab_offset, const int64_t *k, const double *p,
+                            int k_cap, void *out, int64_t ld_out, int32_t *kept_count,
+                            void *workspace, size_t ws_bytes, int flags, int rank, int world,
+                            const qrita_comm *comm, qrita_stream_t stream);
+
+/* The same over an NCCL communicator (ncclComm_t; NCCL is loaded at run time: libnccl.so.2). */
+int qrita_topk_topp_tp(const void *logits, int64_t ld_in, int dtype, int B, int V_shard,
+                       int V_global, int64_t vocab_offset, const int64_t *k, const double *p,
+                       int k_cap, void *out, int64_t ld_out, int32_t *kept_count,
+                       void *workspace, size_t ws_bytes, int flags, int rank, int world,
+                       void *nccl_comm, qrita_stream_t stream);
+
+/* NCCL communicator helpers (a library-owned communicator over the ranks of a job): rank 0 creates
+ * the 128-byte unique id, the job broadcasts it, every rank calls qrita_nccl_comm_init on its own
+ * device.  Return QRITA_OK or QRITA_ENCCL. */
+int qrita_nccl_unique_id(void *id_out /* 128 bytes */);
+int qrita_nccl_comm_init(void **comm_out, int world, const void *id, int rank);
+int qrita_nccl_comm_destroy(void *comm);
+
+/* cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, stream) + stream synchronise (host-staged
+ * exchanges of a qrita_comm implemented outside CUDA, e.g. over gloo). */
+int qrita_copy_sync(void *dst, const void *src, size_t bytes, qrita_stream_t stream);
 
 /* Synchronises `stream`, then reports the first failing row of the last call on this workspace:
  * returns QRITA_OK or QRITA_EINVAL_K / QRITA_EINVAL_P / QRITA_ENONFINITE, and fills *row / *col

@@ -19,7 +19,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
               "-I" + os.path.join(ROOT, "include"), "-I" + CSRC]
 
-SOURCES = ["qrita_capi.cu", "qrita_f32.cu", "qrita_bf16.cu"]
+SOURCES = ["qrita_capi.cu", "qrita_f32.cu", "qrita_bf16.cu", "qrita_tp.cu"]
 
 
 def _nvcc() -> str:
@@ -67,7 +67,7 @@ def build(verbose: bool = False, force: bool = False) -> str:
                 print(out)
     lib = os.path.join(LIB_DIR, "libqrita_b200.so")
     if force or jobs or _stale(lib, objs):
-        cmd = [nvcc, *ARCH, "-shared", "-o", lib, *objs, "-lcudart"]
+        cmd = [nvcc, *ARCH, "-shared", "-o", lib, *objs, "-lcudart", "-ldl"]
         run(cmd)
     return lib
 

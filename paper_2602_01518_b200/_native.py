@@ -22,6 +22,7 @@ NO_DUP = 1 << 3
 INPLACE = 1 << 4
 DEBUG_TIMING = 1 << 6
 STAGED = 1 << 7
+TP_NO_TOPP_ROWS = 1 << 8
 
 OK = 0
 EINVAL_ARG = 1
@@ -36,6 +37,8 @@ EXPORTED_SYMBOLS = (
     "qrita_workspace_bytes", "qrita_workspace_init", "qrita_topk_topp", "qrita_topk_topp_ex", "qrita_topk_topp_idx",
     "qrita_get_status", "qrita_get_timing", "qrita_host_scratch_bytes", "qrita_topk_topp_host",
     "qrita_get_status_host", "qrita_strerror", "qrita_version",
+    "qrita_tp_workspace_bytes", "qrita_topk_topp_tp_comm", "qrita_topk_topp_tp", "qrita_nccl_unique_id",
+    "qrita_nccl_comm_init", "qrita_nccl_comm_destroy", "qrita_copy_sync",
 )
 
 
@@ -97,6 +100,21 @@ def load() -> ctypes.CDLL:
     lib.qrita_topk_topp_host.restype = i32
     lib.qrita_get_status_host.argtypes = [vp, i32, i32, i32, i32, ctypes.POINTER(i32), ctypes.POINTER(i32), vp]
     lib.qrita_get_status_host.restype = i32
+    lib.qrita_tp_workspace_bytes.argtypes = [i32, i32, i32, i32, i32]
+    lib.qrita_tp_workspace_bytes.restype = sz
+    tp_args = [vp, i64, i32, i32, i32, i32, i64, vp, vp, i32, vp, i64, vp, vp, sz, i32, i32, i32, vp, vp]
+    lib.qrita_topk_topp_tp_comm.argtypes = tp_args
+    lib.qrita_topk_topp_tp_comm.restype = i32
+    lib.qrita_topk_topp_tp.argtypes = tp_args
+    lib.qrita_topk_topp_tp.restype = i32
+    lib.qrita_nccl_unique_id.argtypes = [vp]
+    lib.qrita_nccl_unique_id.restype = i32
+    lib.qrita_nccl_comm_init.argtypes = [ctypes.POINTER(vp), i32, ctypes.c_char_p, i32]
+    lib.qrita_nccl_comm_init.restype = i32
+    lib.qrita_nccl_comm_destroy.argtypes = [vp]
+    lib.qrita_nccl_comm_destroy.restype = i32
+    lib.qrita_copy_sync.argtypes = [vp, vp, sz, vp]
+    lib.qrita_copy_sync.restype = i32
     lib.qrita_strerror.argtypes = [i32]
     lib.qrita_strerror.restype = ctypes.c_char_p
     lib.qrita_version.argtypes = []

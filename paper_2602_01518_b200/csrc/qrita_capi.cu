@@ -13,6 +13,7 @@
 #include <vector>
 
 #include "qrita_types.cuh"
+#include "qrita_internal.h"
 
 // ================================================================================================
 // C ABI (include/qrita_b200.h)
@@ -264,18 +265,18 @@ int qrita_topk_topp(const void *logits, int64_t ld_in, int dtype, int B, int V,
 
 }  // extern "C"
 
-namespace {
+namespace qrita {
 
 // qrita_topk_topp_ex with the status / nf_col words optionally placed outside the workspace (the
 // host-buffer pipeline gathers the chunks' status into one [B] block).
 int topk_topp_impl(const void *logits, int64_t ld_in, int dtype, int B, int V, const int64_t *k, const double *p,
                    void *out, int64_t ld_out, int32_t *kept_count, qrita_row_metrics *metrics, void *workspace,
                    size_t ws_bytes, int flags, int sample_size, qrita_stream_t stream, void *prep_done_event,
-                   void *stream_done_event, int32_t *status, int32_t *nf_col, int32_t *kept_idx = NULL,
-                   int64_t ld_idx = 0) {
+                   void *stream_done_event, int32_t *status, int32_t *nf_col, int32_t *kept_idx,
+                   int64_t ld_idx) {
   if (!logits || !k || !p || !workspace) return QRITA_EINVAL_ARG;
   if (!out && !kept_idx) return QRITA_EINVAL_ARG;
-  if (kept_idx && (ld_idx < V || (!kept_count && !metrics))) return QRITA_EINVAL_ARG;
+  if (kept_idx && (ld_idx < 1 || (!kept_count && !metrics))) return QRITA_EINVAL_ARG;
   if (!out) {
     if (flags & QRITA_INPLACE) return QRITA_EINVAL_ARG;
     ld_out = V;
@@ -327,13 +328,14 @@ int topk_topp_impl(const void *logits, int64_t ld_in, int dtype, int B, int V, c
 int scan_status(const int32_t *st, const int32_t *nf, int B, int *row, int *col) {
   if (row) *row = -1;
   if (col) *col = -1;
-  for (int pass = 0; pass < 3; ++pass) {
-    const int bit = pass == 0 ? ST_NONFINITE : pass == 1 ? ST_BAD_K : ST_BAD_P;
+  for (int pass = 0; pass < 4; ++pass) {
+    const int bit = pass == 0 ? ST_NONFINITE : pass == 1 ? ST_BAD_K : pass == 2 ? ST_BAD_P : ST_TP_KCAP;
     for (int r = 0; r < B; ++r) {
       if (st[r] & bit) {
         if (row) *row = r;
         if (col) *col = pass == 0 ? nf[r] : -1;
-        return pass == 0 ? QRITA_ENONFINITE : pass == 1 ? QRITA_EINVAL_K : QRITA_EINVAL_P;
+        return pass == 0 ? QRITA_ENONFINITE : pass == 1 ? QRITA_EINVAL_K : pass == 2 ? QRITA_EINVAL_P
+                                                                                  : QRITA_EINVAL_ARG;
       }
     }
   }
@@ -349,7 +351,7 @@ int read_status(const int32_t *st_dev, const int32_t *nf_dev, int B, int *row, i
   return scan_status(st.data(), st.data() + B, B, row, col);
 }
 
-}  // namespace
+}  // namespace qrita
 
 extern "C" {
 
@@ -366,6 +368,7 @@ int qrita_topk_topp_idx(const void *logits, int64_t ld_in, int dtype, int B, int
                         const double *p, void *out, int64_t ld_out, int32_t *kept_idx, int64_t ld_idx,
                         int32_t *kept_count, qrita_row_metrics *metrics, void *workspace, size_t ws_bytes,
                         int flags, int sample_size, qrita_stream_t stream) {
+  if (kept_idx && ld_idx < V) return QRITA_EINVAL_ARG;  // a row may keep all V columns
   return topk_topp_impl(logits, ld_in, dtype, B, V, k, p, out, ld_out, kept_count, metrics, workspace, ws_bytes,
                         flags, sample_size, stream, NULL, NULL, NULL, NULL, kept_idx, ld_idx);
 }

@@ -38,7 +38,8 @@ constexpr int kWorkBytes = kWorkBytesSearch > kWorkBytesBins ? kWorkBytesSearch 
 static_assert((kMaxTailChunks + 1) * 4 <= kCapC * 8, "chunk offsets alias the candidate array");
 
 enum Mode : int32_t { MODE_INVALID = -1, MODE_PASS = 0, MODE_TOPK = 1, MODE_TOPP = 2, MODE_TOPKP = 3 };
-enum Status : int32_t { ST_BAD_K = 1, ST_BAD_P = 2, ST_NONFINITE = 4 };
+// ST_TP_KCAP: vocab-sharded call, a top-k row's k exceeds the k_cap the caller declared
+enum Status : int32_t { ST_BAD_K = 1, ST_BAD_P = 2, ST_NONFINITE = 4, ST_TP_KCAP = 8 };
 
 // ------------------------------------------------------------------------------------------------
 // Workspace records
