@@ -31,7 +31,7 @@ import numpy as np
 
 __all__ = [
     "stable_desc_order", "nucleus_length", "oracle_keep_row", "oracle_batch", "boundary_of_mask",
-    "mask_from_boundary", "crossing_margin",
+    "mask_from_boundary", "crossing_margin", "oracle_keep_row_nodup",
 ]
 
 
@@ -86,6 +86,33 @@ def oracle_keep_row(row: np.ndarray, k: int, p: float) -> np.ndarray:
     length = nucleus_length(probs_desc, float(p))
     keep[survivors[:length]] = True
     return keep
+
+
+def oracle_keep_row_nodup(row: np.ndarray, k: int, p: float) -> np.ndarray:
+    """Kept mask of the reference PIPELINE with duplication_handling_enabled=False (Table 3 runs C /
+    E): each stage keeps its whole boundary cluster (pipeline.py:47-57 skips the occurrence trim):
+    the top-k stage keeps every z >= z_k (the k-th value of the stable order); the top-p stage
+    renormalises over those survivors with the full-row max (pipeline.py:226-239) and keeps every
+    survivor >= the value at which the exactly rounded prefix mass crosses p (pivot_search.py:159-196
+    keeps all when even the whole set falls short)."""
+    row = np.asarray(row)
+    v = row.shape[0]
+    z = row.astype(np.float64)
+    keep = np.ones(v, dtype=bool)
+    order = stable_desc_order(row)
+    if k < v:
+        keep = z >= z[order[k - 1]]
+    if p == 1.0:
+        return keep
+    m = float(z.max())
+    surv = np.nonzero(keep)[0]                      # index order
+    e = np.exp(z[surv] - m)
+    denom = float(e.sum())
+    probs = e / denom
+    o = np.argsort(-z[surv], kind="stable")
+    length = nucleus_length(probs[o], float(p))
+    zb = z[surv][o[length - 1]]
+    return keep & (z >= zb)
 
 
 def oracle_batch(x: np.ndarray, k, p):

@@ -202,6 +202,47 @@ def configs():
         json.dump(meta, fh, indent=1)
 
 
+ABLATIONS = {  # Table 3 runs of cli.py:157-166 that change the pipeline's configuration
+    "C": dict(search_kind="quaternary", duplication_handling_enabled=False),
+    "D": dict(search_kind="binary"),
+    "E": dict(search_kind="binary", duplication_handling_enabled=False),
+    "F": dict(search_kind="quaternary", force_fallback=True),
+    "H": dict(search_kind="quaternary", sigma_trunc_enabled=False),
+}
+
+
+def ablation():
+    """The reference PIPELINE's own outputs (sigmatop.run_batch, engine.py:82-113) under the
+    ablation configurations of Table 3 (cli.py:157-166).  dup_handling=False (runs C, E) changes the
+    answer — the whole boundary cluster is kept at each stage (pipeline.py:47-57) — so those
+    kept sets come from the pipeline, not the oracle; D / F / H must equal the oracle."""
+    data, meta = {}, []
+    for ki, kind in enumerate(("gaussian", "quantized")):
+        for vi, vocab in enumerate((1000, 4096, 32768)):
+            b = {1000: 16, 4096: 8, 32768: 4}[vocab]
+            seed = 500 + ki * 10 + vi
+            x = synth(kind, b, vocab, seed)
+            rng = np.random.default_rng(seed)
+            cells = [("k=10", np.full(b, 10), np.full(b, 1.0)), ("k=50", np.full(b, 50), np.full(b, 1.0)),
+                     ("p=0.7", np.full(b, vocab), np.full(b, 0.7)), ("p=0.9", np.full(b, vocab), np.full(b, 0.9)),
+                     ("combined", np.full(b, 50), np.full(b, 0.9)),
+                     ("rand", rng.integers(1, min(vocab, 1024) + 1, size=b), rng.uniform(0.3, 0.99, b))]
+            for label, kk, pp in cells:
+                kk, pp = kk.astype(np.int64), pp.astype(np.float64)
+                key = f"{kind}|{vocab}|{label}"
+                data[key + "|k"], data[key + "|p"] = kk, pp
+                for run, cfg in ABLATIONS.items():
+                    outs, _ = run_batch(LogitBatch(x), TruncTargets(kk, pp), EngineConfig(**cfg))
+                    trip = np.array([triplet(x[i], ~np.isneginf(outs[i])) for i in range(b)], dtype=np.int64)
+                    data[key + "|" + run] = trip
+                meta.append({"key": key, "kind": kind, "vocab": vocab, "batch": b, "seed": seed, "kw": {},
+                             "sha256": sha256(x)})
+    np.savez_compressed(os.path.join(HERE, "ablation.npz"), **data)
+    with open(os.path.join(HERE, "ablation_meta.json"), "w") as fh:
+        json.dump({"runs": ABLATIONS, "cells": meta}, fh)
+    print("ablation cells:", len(meta), "x", len(ABLATIONS), "runs")
+
+
 if __name__ == "__main__":
     which = sys.argv[1:] or ["kats", "exhaustive", "corpus", "configs"]
     for w in which:

@@ -80,3 +80,30 @@ def same_bits(a: np.ndarray, b: np.ndarray) -> np.ndarray:
     a = np.asarray(a, dtype=np.float32)
     b = np.asarray(b, dtype=np.float32)
     return (a.view(np.uint32) == b.view(np.uint32)) | (np.isneginf(a) & np.isneginf(b))
+
+
+def ablation():
+    """Yields (key, x, k, p, {run: trip}) per cell of tests/golden/ablation.npz (the reference pipeline
+    under Table 3's ablation configurations), inputs regenerated from seeds."""
+    with open(os.path.join(GOLDEN, "ablation_meta.json")) as fh:
+        meta = json.load(fh)
+    z = np.load(os.path.join(GOLDEN, "ablation.npz"))
+    runs = list(meta["runs"])
+    cache = {}
+    for m in meta["cells"]:
+        sk = (m["kind"], m["vocab"], m["batch"], m["seed"])
+        if sk not in cache:
+            x = synth(m["kind"], m["batch"], m["vocab"], m["seed"])
+            assert sha256(x) == m["sha256"], f"input drift for {m['key']}"
+            cache[sk] = x
+        key = m["key"]
+        yield key, cache[sk], z[key + "|k"], z[key + "|p"], {r: z[key + "|" + r] for r in runs}
+
+
+ABLATION_FLAGS = {  # Table 3 run -> this build's TruncFlags keyword arguments
+    "C": dict(dup_handling=False),
+    "D": dict(search="binary"),
+    "E": dict(search="binary", dup_handling=False),
+    "F": dict(force_fallback=True),
+    "H": dict(use_sigma_trunc=False),
+}

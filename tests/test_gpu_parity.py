@@ -80,6 +80,17 @@ def test_ablation_flags_same_output(cuda_device, flags):
         assert_rows(x, out, kept, trip, f"{key} {flags}")
 
 
+@pytest.mark.parametrize("run_id", ["C", "D", "E", "F", "H"])
+@pytest.mark.parametrize("staged", [False, True])
+def test_table3_ablations_vs_reference_pipeline(cuda_device, run_id, staged):
+    """Table 3 runs C-H (cli.py:157-166) against the reference PIPELINE's own outputs under the same
+    EngineConfig (tests/golden/ablation.npz): C / E (no duplicate handling) keep whole boundary
+    clusters, D / F / H are exact."""
+    for key, x, k, p, runs in G.ablation():
+        out, kept, _ = run(x, k, p, staged=staged, **G.ABLATION_FLAGS[run_id])
+        assert_rows(x, out, kept, runs[run_id], f"{key} run {run_id} staged={staged}")
+
+
 @pytest.mark.parametrize("name", ["cfg1", "cfg2", "cfg3", "cfg4", "cfg5"])
 def test_configs_full_size(cuda_device, name):
     x, k, p, dtype, trip, mets = G.config(name)

@@ -6,7 +6,7 @@ import numpy as np
 import pytest
 
 from oracle.qrita_oracle import (boundary_of_mask, crossing_margin, mask_from_boundary,
-                                 oracle_batch, oracle_keep_row)
+                                 oracle_batch, oracle_keep_row, oracle_keep_row_nodup)
 from oracle.synth import bf16_bits_to_f32, to_bf16_bits
 from tests import golden_io as G
 
@@ -84,3 +84,20 @@ def test_bf16_rounding_matches_torch():
     ref = torch.from_numpy(x).to(torch.bfloat16).view(torch.int16).numpy().view(np.uint16)
     assert np.array_equal(ours, ref)
     assert np.array_equal(bf16_bits_to_f32(ours), torch.from_numpy(x).to(torch.bfloat16).float().numpy())
+
+
+def test_ablation_goldens_pin_the_oracles():
+    """Table 3 ablations: runs D / F / H (binary search, forced fallback, no sigma) leave the answer
+    unchanged (the oracle's); runs C / E (no duplicate handling) follow the pipeline's whole-cluster
+    rule, restated by oracle_keep_row_nodup."""
+    n = 0
+    for key, x, k, p, runs in G.ablation():
+        for i in range(x.shape[0]):
+            exact = oracle_keep_row(x[i], int(k[i]), float(p[i]))
+            nodup = oracle_keep_row_nodup(x[i], int(k[i]), float(p[i]))
+            for run, trip in runs.items():
+                want = G.keep_from_trip(x[i], trip[i])
+                got = nodup if run in ("C", "E") else exact
+                assert np.array_equal(got, want), (key, run, i)
+                n += 1
+    assert n >= 5 * 150
