@@ -219,6 +219,16 @@ int qrita_nccl_comm_destroy(void *comm);
  * exchanges of a qrita_comm implemented outside CUDA, e.g. over gloo). */
 int qrita_copy_sync(void *dst, const void *src, size_t bytes, qrita_stream_t stream);
 
+/* The reference's sigma_trunc primitives (pkg/src/sigmatop/sigma_trunc.py):
+ *   qrita_sigma_table  <- TOPK_TABLE / TOPP_TABLE (tables.py:13-57): copies the 200 embedded entries
+ *                         of kind 0 (top-k) or 1 (top-p) into HOST out[n >= 200]; no CUDA call.
+ *   qrita_row_stats    <- row_stats (sigma_trunc.py:69-82): DEVICE out[B][2] = (mu, sigma) of the
+ *                         first min(sample_size, V) entries of every row, numpy's pairwise sums bit
+ *                         for bit; stream-ordered. */
+int qrita_sigma_table(int kind, double *out, int n);
+int qrita_row_stats(const void *logits, int64_t ld, int dtype, int B, int V, int sample_size, double *out,
+                    qrita_stream_t stream);
+
 /* Synchronises `stream`, then reports the first failing row of the last call on this workspace:
  * returns QRITA_OK or QRITA_EINVAL_K / QRITA_EINVAL_P / QRITA_ENONFINITE, and fills *row / *col
  * (col = first non-finite column, or -1). */

@@ -38,7 +38,8 @@ EXPORTED_SYMBOLS = (
     "qrita_get_status", "qrita_get_timing", "qrita_host_scratch_bytes", "qrita_topk_topp_host",
     "qrita_get_status_host", "qrita_strerror", "qrita_version",
     "qrita_tp_workspace_bytes", "qrita_topk_topp_tp_comm", "qrita_topk_topp_tp", "qrita_nccl_unique_id",
-    "qrita_nccl_comm_init", "qrita_nccl_comm_destroy", "qrita_copy_sync",
+    "qrita_nccl_comm_init", "qrita_nccl_comm_destroy", "qrita_copy_sync", "qrita_sigma_table",
+    "qrita_row_stats",
 )
 
 
@@ -115,6 +116,10 @@ def load() -> ctypes.CDLL:
     lib.qrita_nccl_comm_destroy.restype = i32
     lib.qrita_copy_sync.argtypes = [vp, vp, sz, vp]
     lib.qrita_copy_sync.restype = i32
+    lib.qrita_sigma_table.argtypes = [i32, vp, i32]
+    lib.qrita_sigma_table.restype = i32
+    lib.qrita_row_stats.argtypes = [vp, i64, i32, i32, i32, i32, vp, vp]
+    lib.qrita_row_stats.restype = i32
     lib.qrita_strerror.argtypes = [i32]
     lib.qrita_strerror.restype = ctypes.c_char_p
     lib.qrita_version.argtypes = []

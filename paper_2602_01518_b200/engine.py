@@ -7,6 +7,8 @@ validated for compatibility (output never depended on it, test_acceptance.py:177
 """
 from __future__ import annotations
 
+import csv
+import ctypes
 import statistics
 import time
 from dataclasses import dataclass, field
@@ -15,6 +17,7 @@ from typing import Callable, List, Optional
 import numpy as np
 import torch
 
+from . import _native as N
 from . import ops
 from .core import LogitBatch, RowMetrics, Tolerances, TruncTargets, _is_tensor, validate_batch
 
@@ -200,12 +203,13 @@ def verify_batch(batch: LogitBatch, targets: TruncTargets, config: EngineConfig,
                  reference: Optional[Callable] = None) -> List[Divergence]:
     """Differential check (engine.py:116-136): this build against a reference row function
     `reference(row, k, p) -> masked_row` (numpy).  Default reference: the exact sort-based GPU
-    selection `sort_select` (an independent code path: stable sort + exact prefix masses)."""
+    selection `sort_select` (an independent code path: stable sort + exact prefix masses), under the
+    config's duplicate-handling semantics."""
     _check_inputs(batch, targets)
     got, _ = run_batch(batch, targets, config)
     got = got if not _is_tensor(got) else got.float().cpu().numpy()
     if reference is None:
-        want = sort_select(batch, targets)
+        want = sort_select(batch, targets, dup_handling=config.duplication_handling_enabled)
         want = want if not _is_tensor(want) else want.float().cpu().numpy()
     else:
         xs = batch.values if not _is_tensor(batch.values) else batch.values.float().cpu().numpy()
@@ -264,14 +268,54 @@ def synth_batch(kind: str, batch_size: int, vocab_size: int, seed: int, **params
 
 
 def sort_select(batch: LogitBatch, targets: TruncTargets, use_sigma_trunc: bool = False,
-                sample_size: int = ops.DEFAULT_SAMPLE_SIZE):
+                sample_size: int = ops.DEFAULT_SAMPLE_SIZE, dup_handling: bool = True):
     """Sort-based selection (engine.py:183-205), exact, on the GPU: stable descending sort, top-k
     prefix, fp64 softmax over the survivors, exact prefix masses (sortsel.py).  Independent of the
-    pivot-search kernels; used as verify_batch's default reference and as a bench baseline."""
+    pivot-search kernels; verify_batch's default reference and Table 3 runs I / J.
+
+    use_sigma_trunc=True (run I): rows with k != V whose sigma pre-filter hits (count > k,
+    sigma_trunc.py:127-138) sort only their outliers — the entries above t = mu + delta_adj * sigma,
+    in index order — exactly as the reference does (engine.py:190-201); the answer is the same.
+    dup_handling=False: the pipeline's whole-cluster rule (Table 3 runs C / E) instead of the
+    oracle's."""
+    from . import sigma as S
     from .sortsel import exact_sort_topk_topp
     _check_inputs(batch, targets)
     x, k, p = _device_inputs(batch, targets)
-    out = exact_sort_topk_topp(x, k, p)
+    b, v = x.shape
+    out = None
+    if use_sigma_trunc:
+        kk = k.cpu().numpy()
+        rows = [i for i in range(b) if kk[i] != v]
+        if rows:
+            xs = x[rows].contiguous()
+            stats = torch.empty((len(rows), 2), dtype=torch.float64, device=x.device)
+            st = torch.cuda.current_stream(x.device)
+            rc = N.load().qrita_row_stats(ctypes.c_void_p(xs.data_ptr()), v, ops._DTYPES[xs.dtype], len(rows), v,
+                                          int(sample_size), ctypes.c_void_p(stats.data_ptr()),
+                                          ctypes.c_void_p(st.cuda_stream))
+            if rc != N.OK:
+                raise RuntimeError(f"qrita_row_stats failed: {N.strerror(rc)}")
+            mu_sig = stats.cpu().numpy()
+            out = torch.empty_like(x)
+            done = np.zeros(b, dtype=bool)
+            for j, i in enumerate(rows):
+                delta = S.lookup_delta_topk(int(kk[i]), v)
+                t = S.threshold_from(S.GaussianStats(float(mu_sig[j, 0]), float(mu_sig[j, 1]), sample_size), delta).t
+                z = x[i].to(torch.float64)
+                idx = torch.nonzero(z > t, as_tuple=True)[0]
+                if idx.numel() > int(kk[i]):                 # hit: sort the outliers only
+                    sub = exact_sort_topk_topp(x[i, idx].unsqueeze(0), k[i:i + 1], p[i:i + 1],
+                                               dup_handling=dup_handling)[0]
+                    out[i].fill_(float("-inf"))
+                    out[i, idx] = sub
+                    done[i] = True
+            rest = np.nonzero(~done)[0]
+            if rest.size:
+                ri = torch.as_tensor(rest, device=x.device)
+                out[ri] = exact_sort_topk_topp(x[ri], k[ri], p[ri], dup_handling=dup_handling)
+    if out is None:
+        out = exact_sort_topk_topp(x, k, p, dup_handling=dup_handling)
     return out if _is_tensor(batch.values) else out.cpu().numpy()
 
 
@@ -305,3 +349,35 @@ def bench(batch: LogitBatch, targets: TruncTargets, config: EngineConfig, repeat
                 "rows_per_s": batch.batch_size / (med / 1e9)}
 
     return [row("pipeline", pipe), row("sort_oracle", oracle)]
+
+
+def report_row(run_id: str, batch: LogitBatch, targets: TruncTargets, config: EngineConfig,
+               report: BatchReport) -> dict:
+    """One aggregate CSV row in the fixed report schema (engine.py:240-262).  The search-iteration
+    means are this build's integer-key pivot passes (RowMetrics note in core.py)."""
+    kk = targets.k.cpu().numpy() if _is_tensor(targets.k) else np.asarray(targets.k)
+    pp = targets.p.cpu().numpy() if _is_tensor(targets.p) else np.asarray(targets.p)
+    ks, ps = np.unique(kk), np.unique(pp)
+    return {
+        "run_id": run_id, "B": batch.batch_size, "V": batch.vocab_size,
+        "k": int(ks[0]) if ks.shape[0] == 1 else "rand",
+        "p": float(ps[0]) if ps.shape[0] == 1 else "rand",
+        "search_kind": config.search_kind,
+        "trunc_enabled": config.sigma_trunc_enabled and not config.force_fallback,
+        "dup_enabled": config.duplication_handling_enabled,
+        "hit_rate": report.hit_rate, "mean_outliers": report.mean_outliers,
+        "mean_prob_sum": report.mean_prob_sum, "mean_iters_k": report.mean_iters_k,
+        "mean_iters_p": report.mean_iters_p, "wall_ms": report.wall_time_ns / 1e6,
+        "rows_per_s": report.rows_per_second,
+    }
+
+
+def write_report_csv(rows: List[dict], path, columns: Optional[List[str]] = None) -> None:
+    """CSV in the reference's fixed schema (engine.py:265-269); `columns` may append extra columns
+    (the B200 bench adds the parity tag of each run)."""
+    cols = columns or REPORT_COLUMNS
+    with open(path, "w", newline="") as fh:
+        w = csv.DictWriter(fh, fieldnames=cols, lineterminator="\n")
+        w.writeheader()
+        for r in rows:
+            w.writerow({c: r.get(c, "") for c in cols})

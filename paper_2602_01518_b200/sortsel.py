@@ -81,8 +81,10 @@ def _round_threshold(p: float) -> int:
 
 @torch.no_grad()
 def exact_sort_topk_topp(x: torch.Tensor, k: torch.Tensor, p: torch.Tensor,
-                         rows_per_step: int = 64) -> torch.Tensor:
-    """Exact reference semantics via a stable sort; returns masked logits in x's dtype."""
+                         rows_per_step: int = 64, dup_handling: bool = True) -> torch.Tensor:
+    """Exact reference semantics via a stable sort; returns masked logits in x's dtype.
+    dup_handling=False: the reference pipeline's whole-cluster rule (pipeline.py:47-57; Table 3
+    runs C / E): each stage keeps every copy of its boundary value."""
     b, v = x.shape
     out = torch.full_like(x, float("-inf"))
     kk = k.tolist()
@@ -98,6 +100,8 @@ def exact_sort_topk_topp(x: torch.Tensor, k: torch.Tensor, p: torch.Tensor,
             if ki == v and pi == 1.0:
                 out[r] = x[r]
                 continue
+            if not dup_handling and ki < v:   # the whole k-th cluster survives
+                ki = int((zs[i] >= zs[i, ki - 1]).sum())
             if pi == 1.0:
                 idx = order[i, :ki]
                 out[r, idx] = x[r, idx]
@@ -114,6 +118,8 @@ def exact_sort_topk_topp(x: torch.Tensor, k: torch.Tensor, p: torch.Tensor,
                 L = ki
             else:
                 L = int(torch.nonzero(_ge(pref, t_p))[0, 0]) + 1
+                if not dup_handling:          # and the whole crossing cluster
+                    L = int((zs[i, :ki] >= zs[i, L - 1]).sum())
             idx = order[i, :L]
             out[r, idx] = x[r, idx]
     return out

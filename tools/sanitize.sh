@@ -10,7 +10,7 @@ CASES=${*:-"cfg1 cfg2 cfg3 mixed staged idx binary fallback nosigma tp host"}
 for tool in memcheck racecheck synccheck initcheck; do
   for c in $CASES; do
     log=gpurun_out/sanitize/${tool}_${c}.log
-    timeout 1200 compute-sanitizer --tool $tool --kernel-name regex:'qrita|tp_' --print-limit 20 \
+    timeout 1200 compute-sanitizer --tool $tool --kernel-name kns=qrita --print-limit 20 \
       python tools/sanit.py $c > $log 2>&1
     rc=$?
     echo "$tool $c rc=$rc $(grep -h 'ERROR SUMMARY\|RACECHECK SUMMARY' $log | tr '\n' ' ') $(grep -c '^ok' $log) ok" \
