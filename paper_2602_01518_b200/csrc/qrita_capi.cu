@@ -303,6 +303,7 @@ int topk_topp_impl(const void *logits, int64_t ld_in, int dtype, int B, int V, c
   P.kept_idx = kept_idx; P.ld_idx = ld_idx;
   P.plans = (RowPlan *)(ws + L.plans);
   P.agg = (RowAgg *)(ws + L.agg);
+  P.handled = (int32_t *)(ws + L.handled);
   P.cand_bits = (uint32_t *)(ws + L.cand_bits);
   P.cand_idx = (uint32_t *)(ws + L.cand_idx);
   P.status = status ? status : (int32_t *)(ws + L.status);

@@ -197,9 +197,11 @@ __global__ void __launch_bounds__(kFusedThreads, 2) qrita_fused(Params P) {
     mbar_fence_init();
   }
   __syncthreads();
+  if (P.topp16) pdl_wait();  // qrita_topp16 (the previous kernel) has written `handled`
   const unsigned long long pol = l2_evict_first_policy();
   uint32_t g0 = 0u;  // chunks of this CTA's earlier rows: the ring's stage sequence
   for (int row = blockIdx.x; row < P.B; row += gridDim.x) {
+    if (P.topp16 && P.handled[row]) continue;  // finished by qrita_topp16 (launched just before)
     const T *in = (const T *)P.logits + (size_t)row * P.ld_in;
     // chunk c of the row -> stage (g0 + c) % kRing; seq records the chunk before its copy is issued
     auto issue = [&](int c) {
@@ -297,7 +299,7 @@ __global__ void __launch_bounds__(kFusedThreads, 2) qrita_fused(Params P) {
 constexpr size_t kFusedDynSmem = (size_t)kCapXF * 8 + (size_t)kRing * kStageBytes;
 
 template <typename T, int NP>
-static cudaError_t launch_fused(const Params &P, cudaStream_t st) {
+static cudaError_t launch_fused(const Params &P, cudaStream_t st, bool pdl = false) {
   static int grid_caps[kMaxDevices] = {};  // per instantiation and device
   int grid_cap = 0;
   cudaError_t e = per_device_once(grid_caps, [](int dev, int &cap) {
@@ -320,8 +322,21 @@ static cudaError_t launch_fused(const Params &P, cudaStream_t st) {
     const int bal = (P.B + per - 1) / per;
     if (4 * bal >= 3 * grid_cap) grid = bal;
   }
-  qrita_fused<T, NP><<<grid, kFusedThreads, kFusedDynSmem, st>>>(P);
-  return cudaGetLastError();
+  if (!pdl) {
+    qrita_fused<T, NP><<<grid, kFusedThreads, kFusedDynSmem, st>>>(P);
+    return cudaGetLastError();
+  }
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3(kFusedThreads);
+  cfg.dynamicSmemBytes = kFusedDynSmem;
+  cfg.stream = st;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, qrita_fused<T, NP>, P);
 }
 
 }  // namespace qrita

@@ -34,6 +34,7 @@
 #include "qrita_types.cuh"
 #include "qrita_fused.cuh"
 #include "qrita_staged.cuh"
+#include "qrita_topp16.cuh"
 
 namespace qrita {
 
@@ -44,7 +45,17 @@ static cudaError_t launch_all(const Params &P, cudaStream_t st, bool vec, cudaEv
   const bool fused_ok = vec && ((size_t)P.V * sizeof(T)) % 16 == 0 && !(P.flags & QRITA_STAGED);
   if (fused_ok) {
     if (prep_done) cudaEventRecord(prep_done, st);
-    cudaError_t e = (P.flags & QRITA_SEARCH_BINARY) ? launch_fused<T, 1>(P, st) : launch_fused<T, 3>(P, st);
+    Params PF = P;
+    if constexpr (sizeof(T) == 2) {
+      if (P.V >= kStageBytes) {
+        // bf16: top-p-only rows go to the two-CTA histogram kernel first; the fused kernel skips them
+        cudaError_t e = launch_topp16(P, st);
+        if (e != cudaSuccess) return e;
+        PF.topp16 = 1;
+      }
+    }
+    const bool pdl = PF.topp16 != 0;
+    cudaError_t e = (P.flags & QRITA_SEARCH_BINARY) ? launch_fused<T, 1>(PF, st, pdl) : launch_fused<T, 3>(PF, st, pdl);
     if (e == cudaSuccess && stream_done) e = cudaEventRecord(stream_done, st);
     return e;
   }

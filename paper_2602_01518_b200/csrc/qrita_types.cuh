@@ -105,6 +105,8 @@ struct Params {
   uint32_t *cand_idx;       // [B][xcap] their column indices
   int32_t *status;
   int32_t *nf_col;
+  int32_t *handled;         // [B] row finished by qrita_topp16 (bf16 top-p-only rows)
+  int topp16;               // qrita_topp16 ran before the fused kernel: skip the rows it handled
   unsigned long long *dbg;  // [B][16] phase timestamps of the row tail (QRITA_DEBUG_TIMING)
   int nchunks;
   int total_items;
@@ -116,7 +118,7 @@ struct Params {
 // record is rewritten by each call (no state carries over), and the status block only depends on
 // B, so qrita_get_status needs no V.
 struct WsLayout {
-  size_t status, nf_col, dbg, plans, agg, cand_bits, cand_idx, total;
+  size_t status, nf_col, dbg, plans, agg, handled, cand_bits, cand_idx, total;
 };
 
 inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
@@ -154,6 +156,7 @@ inline WsLayout ws_layout(int B, int V) {
   L.dbg = off;       off = align_up(off + 128ull * (size_t)B, 256);
   L.plans = off;     off = align_up(off + sizeof(RowPlan) * (size_t)B, 256);
   L.agg = off;       off = align_up(off + sizeof(RowAgg) * (size_t)B, 256);
+  L.handled = off;   off = align_up(off + 4ull * (size_t)B, 256);
   L.cand_bits = off; off = align_up(off + 4ull * (size_t)B * cap, 256);
   L.cand_idx = off;  off = align_up(off + 4ull * (size_t)B * cap, 256);
   L.total = off;

@@ -179,13 +179,14 @@ def _entries_from_sorted(sample_desc: torch.Tensor, kind: str, entries: int) -> 
     n = sample_desc.shape[0]
     dev = sample_desc.device
     if kind == "topk":
-        ranks = torch.ceil(torch.arange(1, entries + 1, dtype=torch.float64, device=dev) / entries * n)
-        idx = torch.clamp(ranks.to(torch.int64) - 1, max=n - 1)
+        # the ranks are host arithmetic, exactly the reference's expression (sigma_trunc.py:155-157)
+        ranks = np.ceil(np.arange(1, entries + 1) / entries * n)
+        idx = torch.as_tensor(np.minimum(ranks.astype(np.int64) - 1, n - 1), device=dev)
         return sample_desc[idx].cpu().numpy().copy()
     exps = torch.exp(sample_desc - sample_desc[0])
     probs = exps / exps.sum()
     csum = torch.cumsum(probs, 0)
-    targets = torch.arange(1, entries + 1, dtype=torch.float64, device=dev) / entries
+    targets = torch.as_tensor(np.arange(1, entries + 1) / entries, device=dev)
     idx = torch.clamp(torch.searchsorted(csum, targets, side="left"), max=n - 1)
     return sample_desc[idx].cpu().numpy().copy()
 

@@ -111,6 +111,11 @@ def test_generate_tables_gpu(cuda_device):
     idx = np.minimum(np.ceil(np.arange(1, 201) / 200 * 200_000).astype(np.int64) - 1, 200_000 - 1)
     assert np.array_equal(ek, s[idx])
     ep = Q.generate_table_entries("topp", 200_000, 0)
-    assert np.max(np.abs(ep[:191] - Q.TOPP_TABLE.entries[:191])) < 0.1
+    exps = np.exp(s - s[0])
+    csum = np.cumsum(exps / exps.sum())
+    want = s[np.minimum(np.searchsorted(csum, np.arange(1, 201) / 200, side="left"), 200_000 - 1)]
+    # the GPU's cumulative sums round differently from numpy's sequential cumsum: an entry may move to
+    # the neighbouring sample where two cumulative masses straddle a target within a few ulps
+    assert (ep == want).mean() > 0.95 and np.max(np.abs(ep - want)) < 1e-3
     tk, tp = Q.profile_tables(torch.randn(8, 50000, device="cuda"))
     assert abs(tk.entries[100] - 0.0) < 0.05 and tp.kind == "topp"

@@ -4,7 +4,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
 import paper_2602_01518_b200 as Q
 import bench
-x, k, p, dtype, desc = bench.workload("cfg2")
+x, k, p, dtype, desc, *_ = bench.workload("cfg2")
 xt = torch.from_numpy(x).cuda(); kt, pt = torch.from_numpy(k).cuda(), torch.from_numpy(p).cuda()
 out = torch.empty_like(xt)
 fl = torch.empty(64 << 20, device="cuda"); sink = torch.empty(1, device="cuda")

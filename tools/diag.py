@@ -59,7 +59,7 @@ else:
 if len(sys.argv) > 1 and sys.argv[1] == "stats":
     import bench
     for cfg in sys.argv[2:]:
-        x, k, p, dtype, desc = bench.workload(cfg)
+        x, k, p, dtype, desc, *_ = bench.workload(cfg)
         tdt = torch.bfloat16 if dtype == "bf16" else torch.float32
         xt = torch.from_numpy(x).cuda().to(tdt)
         met = Q.ops.metrics_buffer(x.shape[0], xt.device)
@@ -74,7 +74,7 @@ if len(sys.argv) > 1 and sys.argv[1] == "wtiming":
     import bench, ctypes
     from paper_2602_01518_b200 import _native as N
     for cfg in sys.argv[2:]:
-        x, k, p, dtype, desc = bench.workload(cfg)
+        x, k, p, dtype, desc, *_ = bench.workload(cfg)
         xt = torch.from_numpy(x).cuda()
         kt, pt = torch.from_numpy(k).cuda(), torch.from_numpy(p).cuda()
         fl = Q.TruncFlags(debug_timing=True)
@@ -103,7 +103,7 @@ if len(sys.argv) > 1 and sys.argv[1] == "timing":
     import bench, ctypes
     from paper_2602_01518_b200 import _native as N
     for cfg in sys.argv[2:]:
-        x, k, p, dtype, desc = bench.workload(cfg)
+        x, k, p, dtype, desc, *_ = bench.workload(cfg)
         tdt = torch.bfloat16 if dtype == "bf16" else torch.float32
         xt = torch.from_numpy(x).cuda().to(tdt)
         kt, pt = torch.from_numpy(k).cuda(), torch.from_numpy(p).cuda()
@@ -143,7 +143,7 @@ if len(sys.argv) > 1 and sys.argv[1] == "ftiming":
     import bench, ctypes
     from paper_2602_01518_b200 import _native as N
     for cfg in sys.argv[2:]:
-        x, k, p, dtype, desc = bench.workload(cfg)
+        x, k, p, dtype, desc, *_ = bench.workload(cfg)
         tdt = torch.bfloat16 if dtype == "bf16" else torch.float32
         xt = torch.from_numpy(x).cuda().to(tdt)
         kt, pt = torch.from_numpy(k).cuda(), torch.from_numpy(p).cuda()
@@ -189,7 +189,7 @@ if len(sys.argv) > 1 and sys.argv[1] == "smid":
     import bench, ctypes
     from paper_2602_01518_b200 import _native as N
     cfg = sys.argv[2] if len(sys.argv) > 2 else "cfg2"
-    x, k, p, dtype, desc = bench.workload(cfg)
+    x, k, p, dtype, desc, *_ = bench.workload(cfg)
     xt = torch.from_numpy(x).cuda()
     kt, pt = torch.from_numpy(k).cuda(), torch.from_numpy(p).cuda()
     fl = Q.TruncFlags(debug_timing=True)
@@ -219,7 +219,7 @@ if len(sys.argv) > 1 and sys.argv[1] == "smidmap":
     # per-SM stream time over several runs: are slow rows tied to particular SMs?
     import bench, ctypes
     from paper_2602_01518_b200 import _native as N
-    x, k, p, dtype, desc = bench.workload("cfg2")
+    x, k, p, dtype, desc, *_ = bench.workload("cfg2")
     xt = torch.from_numpy(x).cuda()
     kt, pt = torch.from_numpy(k).cuda(), torch.from_numpy(p).cuda()
     fl = Q.TruncFlags(debug_timing=True)
@@ -246,3 +246,28 @@ if len(sys.argv) > 1 and sys.argv[1] == "smidmap":
     two = n / 8 == 2
     print("2-row SMs: smid<74 mean", round(mean[two & (np.arange(148) < 74)].mean(), 2), " smid>=74 mean", round(mean[two & (np.arange(148) >= 74)].mean(), 2))
     print("per-SM std over 2-row SMs", round(mean[two].std(), 2))
+
+if len(sys.argv) > 1 and sys.argv[1] == "t16timing":
+    # qrita_topp16 (bf16 top-p-only rows): per-row phase stamps of the cluster's CTA 0
+    import bench, ctypes
+    from paper_2602_01518_b200 import _native as N
+    x, k, p, dtype, desc, *_ = bench.workload("cfg3")
+    xt = torch.from_numpy(x).cuda().to(torch.bfloat16)
+    kt, pt = torch.from_numpy(k).cuda(), torch.from_numpy(p).cuda()
+    fl = Q.TruncFlags(debug_timing=True)
+    st = torch.cuda.current_stream()
+    ws = Q.ops.workspace_for(xt.device, st)
+    for _ in range(3):
+        Q.topk_topp(xt, kt, pt, flags=fl)
+    ptr, _ = ws.get(0, st)
+    B = x.shape[0]
+    buf = (ctypes.c_ulonglong * (16 * B))()
+    N.load().qrita_get_timing(ctypes.c_void_p(ptr), B, buf, ctypes.c_void_p(st.cuda_stream))
+    a = np.frombuffer(buf, dtype=np.uint64).reshape(B, 16).astype(np.int64)
+    t0 = a[:, 0].min()
+    print(f"cfg3 topp16: start spread {(a[:,0].max()-t0)/1e3:.1f} us, last end {(a[:,6].max()-t0)/1e3:.1f} us")
+    for nm, i, j in (("count", 0, 1), ("sync1", 1, 2), ("merge+D", 2, 3), ("mass", 3, 7), ("suffix", 7, 8),
+                     ("sync3", 8, 9), ("xfind", 9, 10), ("xwarp+s4", 10, 4), ("keptloop", 4, 11), ("kept", 11, 5),
+                     ("output", 5, 6)):
+        d = (a[:, j] - a[:, i]) / 1e3
+        print(f"   {nm:10s} mean {d.mean():7.2f} us  min {d.min():7.2f}  max {d.max():7.2f}")

@@ -6,7 +6,7 @@ import paper_2602_01518_b200 as Q
 import bench
 
 cfg = sys.argv[1] if len(sys.argv) > 1 else "cfg2"
-x_np, k_np, p_np, dtype, desc = bench.workload(cfg)
+x_np, k_np, p_np, dtype, desc, *_ = bench.workload(cfg)
 tdt = torch.bfloat16 if dtype == "bf16" else torch.float32
 x = torch.from_numpy(x_np).cuda().to(tdt)
 k = torch.from_numpy(k_np).cuda(); p = torch.from_numpy(p_np).cuda()

@@ -4,7 +4,7 @@ import numpy as np, torch
 import paper_2602_01518_b200 as Q
 import bench
 for cfg, fl in (("cfg2", None), ("cfg4", None), ("cfg3", None), ("cfg1", None), ("cfg2", Q.TruncFlags(force_fallback=True)), ("cfg2", Q.TruncFlags(use_sigma_trunc=False))):
-    x, k, p, dtype, desc = bench.workload(cfg)
+    x, k, p, dtype, desc, *_ = bench.workload(cfg)
     n = min(x.shape[0], 64)
     tdt = torch.bfloat16 if dtype == "bf16" else torch.float32
     xt = torch.from_numpy(x[:n]).cuda().to(tdt)

@@ -6,7 +6,7 @@ import paper_2602_01518_b200 as Q
 from paper_2602_01518_b200 import _native as N
 import bench
 cfg = sys.argv[1]
-x, k, p, dtype, desc = bench.workload(cfg)
+x, k, p, dtype, desc, *_ = bench.workload(cfg)
 xt = torch.from_numpy(x).cuda()
 kt, pt = torch.from_numpy(k).cuda(), torch.from_numpy(p).cuda()
 met = Q.ops.metrics_buffer(x.shape[0], xt.device)
