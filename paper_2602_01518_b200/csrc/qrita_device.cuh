@@ -194,6 +194,14 @@ __device__ __forceinline__ void pdl_launch_dependents() {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 
+// The ring's chunk-sequence words (written by the producing lane, polled by the consuming warps) are
+// accessed with atomics only: ordered under the memory model and racecheck-clean (a volatile poll is
+// formally a data race).  The distinct-value hash table keeps plain volatile probes on purpose: they
+// are independent loads (the batch of probes is in flight together), a stale probe only sends the
+// thread to the atomicCAS insert, which decides; racecheck reports those probes.
+__device__ __forceinline__ uint32_t ld_relaxed_smem(uint32_t *p) { return atomicOr(p, 0u); }
+__device__ __forceinline__ void st_relaxed_smem(uint32_t *p, uint32_t v) { atomicExch(p, v); }
+
 // Barrier of the row-tail thread group (named barrier 1, kThreads threads), in the non-aligned form
 // (`barrier.sync`; `bar.sync` is `barrier.sync.aligned`).  Callers reach it right after
 // thread-0-only branches and the compiler does not treat inline asm as a barrier, so a warp may

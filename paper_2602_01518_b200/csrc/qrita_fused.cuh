@@ -63,7 +63,7 @@ struct FusedSmem {
 // shows g the barrier is in phase n (copy in flight) or n+1 (landed) and the parity is unambiguous.
 __device__ __forceinline__ void stage_wait(FusedSmem &fs, uint32_t g) {
   const uint32_t slot = g % kRing;
-  while (*(volatile const uint32_t *)&fs.seq[slot] != g) {
+  while (ld_relaxed_smem(&fs.seq[slot]) != g) {
   }
   mbar_wait(&fs.full[slot], (g / kRing) & 1u);
 }
@@ -206,7 +206,7 @@ __global__ void __launch_bounds__(kFusedThreads, 2) qrita_fused(Params P) {
     // chunk c of the row -> stage (g0 + c) % kRing; seq records the chunk before its copy is issued
     auto issue = [&](int c) {
       const uint32_t g = g0 + (uint32_t)c, slot = g % kRing;
-      *(volatile uint32_t *)&fs.seq[slot] = g;
+      st_relaxed_smem(&fs.seq[slot], g);
       const uint32_t bytes = (uint32_t)(min(CE, V - c * CE) * (int)sizeof(T));
       mbar_arrive_expect_tx(&fs.full[slot], bytes);
       tma_load_1d(ring + (size_t)slot * kStageBytes, in + (size_t)c * CE, bytes, &fs.full[slot], pol);

@@ -46,7 +46,7 @@ __device__ __noinline__ DistinctRes distinct_topp(const Params &P, int row, cons
   auto insert_slow = [&](uint32_t key) {
     uint32_t h = (key * 0x9E3779B1u) >> (32u - lg);
     for (uint32_t probe = 0; probe < cap; ++probe) {
-      const uint32_t cur = *(volatile uint32_t *)&tk[h];
+      const uint32_t cur = *(volatile uint32_t *)&tk[h];  // (a stale read only leads to the CAS below)
       if (cur == key) { atomicAdd(&tc[h], 1u); return; }
       if (cur != 0u) { h = (h + 1u) & (cap - 1u); continue; }
       if (sm.dabort) return;

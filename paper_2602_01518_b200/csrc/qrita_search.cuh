@@ -575,6 +575,7 @@ __device__ PRes search_p(const Src &src, uint32_t l, uint32_t r, const Fx &T, co
       tsync();
       return res;
     }
+    tsync();  // every thread has read st.compact above
     if (threadIdx.x == 0 && !st.done) {
       const uint32_t n_in = st.cl - st.cr;
       if ((int)n_in <= R.act_cap_p && 2 * (int)n_in <= src.n) st.compact = 1;
