@@ -364,7 +364,9 @@ def main():
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": traffic,
                 "peak_source": peak_kind,
-                "kernel": "qrita_fused" if kind == "fused" else "qrita_stream",
+                "kernel": ("qrita_topp16 + qrita_fused (top-p-only bf16 rows in qrita_topp16, the fused "
+                           "kernel skips them)" if dtype == "bf16" and kind == "fused" else
+                           "qrita_fused" if kind == "fused" else "qrita_stream"),
                 "kernel_ms": stream_ms, "alg_bytes_per_launch": alg_bytes,
                 "alg_bytes_note": "B*V*sizeof(dtype) read + the same written (SURVEY.md 8d)",
                 "step_frac": alg_bytes / (ms_per_step / 1e3) / 1e9 / peak}
@@ -375,7 +377,7 @@ def main():
         roofline["dram_side_frac"] = roofline["dram_side_gbs"] / peak
     if kind == "staged":
         roofline.update({"prep_ms": prep_ms, "tail_ms_serialised": tail_ms})
-    launches_per_step = 1 if kind == "fused" else 3
+    launches_per_step = (2 if dtype == "bf16" else 1) if kind == "fused" else 3
     # passes over the logits per row (qrita_row_metrics.row_passes): 1 = read once from HBM
     met = Q.ops.metrics_buffer(b, dev)
     Q.topk_topp(x, k, p, out=out, metrics=met, check=True)

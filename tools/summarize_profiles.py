@@ -38,43 +38,52 @@ def launches(cfg):
 
 
 summary = {}
-for cfg in ("cfg2", "cfg4", "cfg3", "cfg1", "cfg2copy"):
+for cfg in ("cfg2", "cfg4", "cfg3", "cfg1", "cfg5", "cfg2copy"):
     try:
         summary[cfg] = launches(cfg)
     except (OSError, StopIteration, KeyError) as e:
         print("skip", cfg, e)
 with open(os.path.join(DST, f"{tag}_launches.json"), "w") as fh:
     json.dump({"how": "ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum "
-                      "--clock-control none -k regex:qrita -s 3 -c 3 python bench.py --config <cfg> "
+                      "--clock-control none -k regex:qrita -s 3 -c 12 python bench.py --config <cfg> "
                       "--steps 3 --warmup 3 --no-extras (cold-cache, serialised: compare shares, not "
                       "absolutes)", "launches": summary}, fh, indent=1)
 
-rep = os.path.join(SRC, "fused_cfg2.ncu-rep")
-if os.path.exists(rep):
+WANT = ["Kernel Name", "gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+        "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "sm__throughput.avg.pct_of_peak_sustained_elapsed",
+        "sm__inst_executed.avg.per_cycle_active", "sm__warps_active.avg.pct_of_peak_sustained_active",
+        "smsp__inst_executed.sum", "launch__registers_per_thread", "launch__grid_size", "launch__block_size",
+        "launch__shared_mem_per_block_dynamic", "launch__shared_mem_per_block_static",
+        "launch__occupancy_limit_registers", "launch__occupancy_limit_shared_mem",
+        "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum", "lts__t_sectors_srcunit_tex_op_read.sum",
+        "smsp__cycles_active.avg"]
+SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+traffic = {}
+for name, cfg, kern, how in (("fused_cfg2", "cfg2", "qrita_fused<float,3>", "-k regex:qrita_fused ... bench.py"),
+                             ("topp16_cfg3", "cfg3", "qrita_topp16", "-k regex:qrita_topp16 ... bench.py --config cfg3")):
+    rep = os.path.join(SRC, f"{name}.ncu-rep")
+    if not os.path.exists(rep):
+        continue
     raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(raw.splitlines()))
     h, units, v = rows[0], rows[1], rows[2]
-    want = ["Kernel Name", "gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
-            "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "sm__throughput.avg.pct_of_peak_sustained_elapsed",
-            "sm__inst_executed.avg.per_cycle_active", "sm__warps_active.avg.pct_of_peak_sustained_active",
-            "smsp__inst_executed.sum", "launch__registers_per_thread", "launch__grid_size", "launch__block_size",
-            "launch__shared_mem_per_block_dynamic", "launch__shared_mem_per_block_static",
-            "launch__occupancy_limit_registers", "launch__occupancy_limit_shared_mem",
-            "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum", "lts__t_sectors_srcunit_tex_op_read.sum",
-            "smsp__cycles_active.avg"]
-    full = {w: [v[h.index(w)], units[h.index(w)]] for w in want if w in h}
-    with open(os.path.join(DST, f"{tag}_ncu_full_fused_cfg2.json"), "w") as fh:
-        json.dump({"how": "ncu --set full --clock-control none --import-source on -k regex:qrita_fused "
-                          "-s 3 -c 1 python bench.py --steps 1 --warmup 3 --no-extras", "metrics": full}, fh, indent=1)
-    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
-    rd = float(full["dram__bytes_read.sum"][0]) * scale[full["dram__bytes_read.sum"][1]]
-    wr = float(full["dram__bytes_write.sum"][0]) * scale[full["dram__bytes_write.sum"][1]]
-    traffic = {"cfg2": {"qrita_main_dram_bytes_per_launch": int(rd + wr), "kernel": "qrita_fused<float,3>",
-                        "dram_read_bytes": int(rd), "dram_write_bytes": int(wr),
-                        "source": f"profiles/{tag}_ncu_full_fused_cfg2.json (ncu --set full, dram__bytes_read.sum + "
-                                  "dram__bytes_write.sum)",
-                        "note": "write bytes still in L2 (dirty) when the kernel ends are written back later "
-                                "and not counted here"}}
+    full = {w: [v[h.index(w)], units[h.index(w)]] for w in WANT if w in h}
+    stalls = {k.replace("smsp__average_warps_issue_stalled_", "").replace("_per_issue_active.ratio", ""):
+              float(v[i]) for i, k in enumerate(h) if k.startswith("smsp__average_warps_issue_stalled_") and
+              k.endswith("_per_issue_active.ratio")}
+    with open(os.path.join(DST, f"{tag}_ncu_full_{name}.json"), "w") as fh:
+        json.dump({"how": f"ncu --set full --clock-control none --import-source on {how} --steps 1 --warmup 3 "
+                          "--no-extras (-s 3 -c 1: one launch, cold caches)", "metrics": full,
+                   "top_stalls_per_issue": dict(sorted(stalls.items(), key=lambda t: -t[1])[:8])}, fh, indent=1)
+    rd = float(full["dram__bytes_read.sum"][0]) * SCALE[full["dram__bytes_read.sum"][1]]
+    wr = float(full["dram__bytes_write.sum"][0]) * SCALE[full["dram__bytes_write.sum"][1]]
+    traffic[cfg] = {"qrita_main_dram_bytes_per_launch": int(rd + wr), "kernel": kern,
+                    "dram_read_bytes": int(rd), "dram_write_bytes": int(wr),
+                    "source": f"profiles/{tag}_ncu_full_{name}.json (ncu --set full, dram__bytes_read.sum + "
+                              "dram__bytes_write.sum)",
+                    "note": "write bytes still in L2 (dirty) when the kernel ends are written back later "
+                            "and not counted here"}
+if traffic:
     with open(os.path.join(DST, "ncu_traffic.json"), "w") as fh:
         json.dump(traffic, fh, indent=1)
 print(json.dumps({k: [(l["kernel"], round(l["us"], 1), round((l["dram_read_bytes"] + l["dram_write_bytes"]) / 1e6, 1)) for l in v] for k, v in summary.items()}, indent=0))
