@@ -452,7 +452,8 @@ __global__ void __launch_bounds__(kT) tp_write(const T *logits, int64_t ld_in, T
                                               int64_t offset, const TpRow *rows, const uint32_t *cgid,
                                               const int32_t *kidx_c, const int32_t *kc_c, int W,
                                               const uint32_t *qbuf, int rank, int world, int32_t *kept_count,
-                                              int32_t *status, const int32_t *tst, int sh) {
+                                              int32_t *status, const int32_t *tst, int sh, int bg_done,
+                                              const int32_t *kidx_s, const int32_t *kc_s, int kmax) {
   extern __shared__ uint32_t bm[];
   __shared__ uint32_t buf[kT / 32];
   __shared__ uint32_t nkept;
@@ -480,7 +481,17 @@ __global__ void __launch_bounds__(kT) tp_write(const T *logits, int64_t ld_in, T
       }
     }
     __syncthreads();
-    for (int c = tid; c < Vr; c += kT) o[c] = (bm[c >> 5] >> (c & 31)) & 1u ? in[c] : ninf;
+    if (bg_done) {
+      // the shard call already wrote the local top-k over a -inf background: only the local
+      // candidates that did not survive globally are cleared
+      const int nl = kc_s[r];
+      for (int i = tid; i < nl; i += kT) {
+        const int c = kidx_s[(size_t)r * kmax + i];
+        if (!((bm[c >> 5] >> (c & 31)) & 1u)) o[c] = ninf;
+      }
+    } else {
+      for (int c = tid; c < Vr; c += kT) o[c] = (bm[c >> 5] >> (c & 31)) & 1u ? in[c] : ninf;
+    }
   } else if (R.mode == MODE_TOPP && R.state == FOUND) {
     uint32_t before = 0u;
     for (int g = 0; g < rank; ++g) before += qbuf[(size_t)r * world + g];
@@ -524,6 +535,7 @@ inline TpLayout tp_layout(int B, int Vr, int world, int k_cap) {
   TpLayout L;
   L.kmax = k_cap < 1 ? 1 : k_cap;
   if (L.kmax > Vr) L.kmax = Vr;
+  L.kmax = (L.kmax + 3) & ~3;  // 16-byte candidate rows: the resolve runs on the fused kernel
   L.W = world * L.kmax;
   L.B4 = (B + 3) & ~3;
   L.send_words = (size_t)L.B4 + 2ull * (size_t)B * (size_t)L.kmax;
@@ -636,10 +648,13 @@ int run_tp(const void *logits, int64_t ld_in, int dtype, int B, int Vr, int Vg, 
   tp_prep<<<(B + 255) / 256, 256, 0, st>>>(B, Vg, Vr, k_cap < 1 ? 1 : k_cap, no_topp ? 1 : 0, k, p, k_loc, p_one,
                                           rows, tst);
   if (cudaGetLastError() != cudaSuccess) return QRITA_ECUDA;
-  // (1) local top-k_loc of the shard: kept columns only (one read of the shard)
-  int rc = topk_topp_impl(logits, ld_in, dtype, B, Vr, k_loc, p_one, nullptr, Vr, (int32_t *)at(L.kc_s), nullptr,
-                          at(L.ws0), L.ws0_bytes, 0, 4096, (qrita_stream_t)st, nullptr, nullptr, nullptr, nullptr,
-                          (int32_t *)at(L.kidx_s), L.kmax);
+  // (1) local top-k_loc of the shard: its kept columns, and — when no row needs the whole shard
+  //     (no top-p-only rows) and the output is a separate buffer — the local top-k over a -inf
+  //     background straight into `out` (the final write then only clears dropped candidates)
+  const bool bg = no_topp && out != logits;
+  int rc = topk_topp_impl(logits, ld_in, dtype, B, Vr, k_loc, p_one, bg ? out : nullptr, bg ? ld_out : Vr,
+                          (int32_t *)at(L.kc_s), nullptr, at(L.ws0), L.ws0_bytes, 0, 4096, (qrita_stream_t)st,
+                          nullptr, nullptr, nullptr, nullptr, (int32_t *)at(L.kidx_s), L.kmax);
   if (rc != QRITA_OK) return rc;
   tp_pack<T><<<B, kT, bm_bytes, st>>>(x, ld_in, Vr, offset, L.kmax, (const int32_t *)at(L.kc_s),
                                       (const int32_t *)at(L.kidx_s), (uint32_t *)at(L.send), L.B4, B);
@@ -677,7 +692,8 @@ int run_tp(const void *logits, int64_t ld_in, int dtype, int B, int Vr, int Vg, 
   tp_write<T><<<B, kT, bm_bytes, st>>>(x, ld_in, (T *)out, ld_out, Vr, offset, rows, (const uint32_t *)at(L.cgid),
                                        (const int32_t *)at(L.kidx_c), (const int32_t *)at(L.kc_c), L.W,
                                        (const uint32_t *)at(L.qbuf), rank, world, kept_count,
-                                       (int32_t *)(ws + L.ws0 + W0.status), tst, sh);
+                                       (int32_t *)(ws + L.ws0 + W0.status), tst, sh, bg ? 1 : 0,
+                                       (const int32_t *)at(L.kidx_s), (const int32_t *)at(L.kc_s), L.kmax);
   return cudaGetLastError() == cudaSuccess ? QRITA_OK : QRITA_ECUDA;
 }
 
