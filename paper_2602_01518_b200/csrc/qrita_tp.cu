@@ -39,7 +39,7 @@
 #include <mutex>
 
 #include "qrita_internal.h"
-#include "qrita_plan.cuh"
+#include "qrita_search.cuh"
 
 namespace qrita {
 namespace tp {
@@ -521,6 +521,71 @@ __global__ void __launch_bounds__(kT) tp_write(const T *logits, int64_t ld_in, T
   if (tid == 0 && kept_count) kept_count[r] = (int32_t)nkept;
 }
 
+// The exact answer on one candidate row (<= kSmallW entries): stable sort by (value desc, position
+// asc) in shared memory, top-k prefix, then — p < 1 — the survivors' exact fixed-point normaliser
+// and prefix masses (oracle.py:70-89): the first prefix whose exactly rounded sum reaches p, all of
+// them when fsum(survivors) <= p.  Writes the kept positions (kidx_c) and their count (kc_c).
+constexpr int kSmallW = 8192;
+
+__global__ void __launch_bounds__(kT) tp_small_resolve(const float *cval, int W, int Wp, const int64_t *k_c,
+                                                      const double *p_c, int32_t *kidx_c, int32_t *kc_c) {
+  extern __shared__ unsigned long long sk[];  // [Wp]
+  __shared__ Fx scan_buf[kThreads / 32];
+  __shared__ uint32_t s_L;
+  const int r = blockIdx.x, tid = threadIdx.x;
+  const float *row = cval + (size_t)r * W;
+  for (int i = tid; i < Wp; i += kT)
+    sk[i] = i < W ? ((unsigned long long)key_of_bits(__float_as_uint(row[i])) << 32) | (0xffffffffu - (uint32_t)i)
+                  : 0ull;
+  __syncthreads();
+  // bitonic sort, descending
+  for (int size = 2; size <= Wp; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int i = tid; i < Wp; i += kT) {
+        const int j = i ^ stride;
+        if (j > i) {
+          const unsigned long long a = sk[i], b = sk[j];
+          const bool desc = (i & size) == 0;
+          if (desc ? a < b : a > b) { sk[i] = b; sk[j] = a; }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  const int k = (int)min((int64_t)W, k_c[r]);
+  const double p = p_c[r];
+  uint32_t L = (uint32_t)k;
+  if (p < 1.0) {
+    const double m = value_of_key((uint32_t)(sk[0] >> 32));
+    const int E = (k + kT - 1) / kT, q0 = tid * E;
+    Fx d = fx_zero();
+    for (int j = 0; j < E; ++j)
+      if (q0 + j < k) d = fx_add(d, fx_from_double(exp(value_of_key((uint32_t)(sk[q0 + j] >> 32)) - m)));
+    Fx D_fx;
+    (void)block_exscan_fx(d, scan_buf, D_fx);
+    const double D = fx_to_double(D_fx);
+    Fx ms = fx_zero();
+    for (int j = 0; j < E; ++j)
+      if (q0 + j < k) ms = fx_add(ms, fx_from_double(exp(value_of_key((uint32_t)(sk[q0 + j] >> 32)) - m) / D));
+    tsync();  // scan_buf reuse
+    Fx total;
+    Fx pre = block_exscan_fx(ms, scan_buf, total);
+    if (tid == 0) s_L = (uint32_t)k;
+    tsync();
+    const Fx Tp = fx_round_threshold(p);
+    for (int j = 0; j < E; ++j) {
+      if (q0 + j < k) {
+        pre = fx_add(pre, fx_from_double(exp(value_of_key((uint32_t)(sk[q0 + j] >> 32)) - m) / D));
+        if (fx_ge(pre, Tp)) { atomicMin(&s_L, (uint32_t)(q0 + j + 1)); break; }
+      }
+    }
+    tsync();
+    L = fx_ge(total, fx_round_threshold(nextafter(p, 2.0))) ? s_L : (uint32_t)k;  // oracle.py:44-46
+  }
+  for (int i = tid; i < (int)L; i += kT) kidx_c[(size_t)r * W + i] = (int32_t)(0xffffffffu - (uint32_t)sk[i]);
+  if (tid == 0) kc_c[r] = (int32_t)L;
+}
+
 // ------------------------------------------------------------------------------------------------
 // workspace layout
 // ------------------------------------------------------------------------------------------------
@@ -664,11 +729,23 @@ int run_tp(const void *logits, int64_t ld_in, int dtype, int B, int Vr, int Vg, 
   tp_merge<<<B, kT, 0, st>>>((const uint32_t *)at(L.recv), L.send_words, L.B4, B, L.kmax, world, L.W, k, p, rows,
                              (float *)at(L.cval), (uint32_t *)at(L.cgid), k_c, p_c);
   if (cudaGetLastError() != cudaSuccess) return QRITA_ECUDA;
-  // (2) the exact answer on the gathered candidates (same on every rank)
-  rc = topk_topp_impl(at(L.cval), L.W, QRITA_DTYPE_F32, B, L.W, k_c, p_c, nullptr, L.W, (int32_t *)at(L.kc_c),
-                      nullptr, at(L.ws1), L.ws1_bytes, 0, 4096, (qrita_stream_t)st, nullptr, nullptr, nullptr, nullptr,
-                      (int32_t *)at(L.kidx_c), L.W);
-  if (rc != QRITA_OK) return rc;
+  // (2) the exact answer on the gathered candidates (same on every rank): a shared-memory sort for
+  //     candidate rows up to kSmallW entries, else the single-GPU kernels
+  if (L.W <= kSmallW) {
+    int wp = 1;
+    while (wp < L.W) wp <<= 1;
+    const size_t sbytes = (size_t)wp * 8;
+    static int optin_small[kMaxDevices] = {};
+    if (sbytes > (48u << 10) && smem_optin(tp_small_resolve, optin_small) != cudaSuccess) return QRITA_ECUDA;
+    tp_small_resolve<<<B, kT, sbytes, st>>>((const float *)at(L.cval), L.W, wp, k_c, p_c, (int32_t *)at(L.kidx_c),
+                                            (int32_t *)at(L.kc_c));
+    if (cudaGetLastError() != cudaSuccess) return QRITA_ECUDA;
+  } else {
+    rc = topk_topp_impl(at(L.cval), L.W, QRITA_DTYPE_F32, B, L.W, k_c, p_c, nullptr, L.W, (int32_t *)at(L.kc_c),
+                        nullptr, at(L.ws1), L.ws1_bytes, 0, 4096, (qrita_stream_t)st, nullptr, nullptr, nullptr,
+                        nullptr, (int32_t *)at(L.kidx_c), L.W);
+    if (rc != QRITA_OK) return rc;
+  }
   // (3) top-p-only rows: exact normaliser, radix boundary search, tie quotas
   if (!no_topp) {
     unsigned long long *dl = (unsigned long long *)at(L.dl), *part = (unsigned long long *)at(L.part),
