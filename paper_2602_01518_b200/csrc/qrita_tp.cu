@@ -205,28 +205,38 @@ __global__ void tp_prep(int B, int Vg, int Vr, int kcap, int no_topp, const int6
 template <typename T>
 __global__ void __launch_bounds__(kT) tp_pack(const T *logits, int64_t ld, int Vr, int64_t offset, int kmax,
                                              const int32_t *kc, const int32_t *kidx, uint32_t *send, int B4,
-                                             int B) {
+                                             int B, int ordered) {
   extern __shared__ uint32_t bm[];
   __shared__ uint32_t buf[kT / 32];
   const int r = blockIdx.x, tid = threadIdx.x;
+  uint32_t *keys = send + B4 + (size_t)r * kmax;
+  uint32_t *gid = send + B4 + (size_t)B * kmax + (size_t)r * kmax;
+  const int cnt = kc[r];
+  const T *row = logits + (size_t)r * ld;
+  if (!ordered) {
+    // the small-row resolve orders ties by global column itself: the list order is free
+    for (int i = tid; i < kmax; i += kT) {
+      const int c = i < cnt ? kidx[(size_t)r * kmax + i] : 0;
+      keys[i] = i < cnt ? key_at(row, c) : 0u;
+      gid[i] = i < cnt ? (uint32_t)(offset + c) : 0xffffffffu;
+    }
+    if (tid == 0) send[r] = (uint32_t)cnt;
+    return;
+  }
   const int nw = (Vr + 31) >> 5;
   for (int i = tid; i < nw; i += kT) bm[i] = 0u;
   __syncthreads();
-  const int cnt = kc[r];
   for (int i = tid; i < cnt; i += kT) {
     const int c = kidx[(size_t)r * kmax + i];
     atomicOr(&bm[c >> 5], 1u << (c & 31));
   }
   __syncthreads();
-  uint32_t *keys = send + B4 + (size_t)r * kmax;
-  uint32_t *gid = send + B4 + (size_t)B * kmax + (size_t)r * kmax;
   const int per = (nw + kT - 1) / kT;
   const int w0 = tid * per, w1 = min(nw, w0 + per);
   uint32_t mine = 0u;
   for (int w = w0; w < w1; ++w) mine += __popc(bm[w]);
   uint32_t total;
   uint32_t pos = cta_exscan(mine, buf, total);
-  const T *row = logits + (size_t)r * ld;
   for (int w = w0; w < w1; ++w) {
     uint32_t m = bm[w];
     while (m) {
@@ -473,7 +483,8 @@ __global__ void __launch_bounds__(kT) tp_write(const T *logits, int64_t ld_in, T
     __syncthreads();
     const int n = kc_c[r];
     for (int i = tid; i < n; i += kT) {
-      const uint32_t g = cgid[(size_t)r * W + kidx_c[(size_t)r * W + i]];
+      const int32_t e = kidx_c[(size_t)r * W + i];
+      const uint32_t g = cgid ? cgid[(size_t)r * W + e] : (uint32_t)e;
       if ((int64_t)g >= offset && (int64_t)g < offset + Vr) {
         const int c = (int)((int64_t)g - offset);
         atomicOr(&bm[c >> 5], 1u << (c & 31));
@@ -521,43 +532,114 @@ __global__ void __launch_bounds__(kT) tp_write(const T *logits, int64_t ld_in, T
   if (tid == 0 && kept_count) kept_count[r] = (int32_t)nkept;
 }
 
-// The exact answer on one candidate row (<= kSmallW entries): stable sort by (value desc, position
+// The exact answer on one candidate row (<= kSmallW entries): sort by (value desc, global column
 // asc) in shared memory, top-k prefix, then — p < 1 — the survivors' exact fixed-point normaliser
 // and prefix masses (oracle.py:70-89): the first prefix whose exactly rounded sum reaches p, all of
-// them when fsum(survivors) <= p.  Writes the kept positions (kidx_c) and their count (kc_c).
-constexpr int kSmallW = 8192;
+// them when fsum(survivors) <= p.  Writes the kept global columns (kidx_c) and their count (kc_c).
+constexpr int kSmallW = 16384;
 
-__global__ void __launch_bounds__(kT) tp_small_resolve(const float *cval, int W, int Wp, const int64_t *k_c,
-                                                      const double *p_c, int32_t *kidx_c, int32_t *kc_c) {
-  extern __shared__ unsigned long long sk[];  // [Wp]
-  __shared__ Fx scan_buf[kThreads / 32];
-  __shared__ uint32_t s_L;
-  const int r = blockIdx.x, tid = threadIdx.x;
-  const float *row = cval + (size_t)r * W;
-  for (int i = tid; i < Wp; i += kT)
-    sk[i] = i < W ? ((unsigned long long)key_of_bits(__float_as_uint(row[i])) << 32) | (0xffffffffu - (uint32_t)i)
-                  : 0ull;
-  __syncthreads();
-  // bitonic sort, descending
-  for (int size = 2; size <= Wp; size <<= 1) {
-    for (int stride = size >> 1; stride > 0; stride >>= 1) {
-      for (int i = tid; i < Wp; i += kT) {
-        const int j = i ^ stride;
-        if (j > i) {
+// Descending bitonic sort of NT * EPT composites: blocked in registers (element t * EPT + j in
+// thread t), strides < EPT in registers, < 32 * EPT through warp shuffles, larger through `sk`.
+template <int NT, int EPT>
+__device__ __forceinline__ void bitonic_desc(unsigned long long *sk) {
+  constexpr int N = NT * EPT;
+  const int tid = threadIdx.x;
+  unsigned long long v[EPT];
+#pragma unroll
+  for (int j = 0; j < EPT; ++j) v[j] = sk[tid * EPT + j];
+  for (int size = 2; size <= N; size <<= 1) {
+    int stride = size >> 1;
+    if (stride >= 32 * EPT) {
+#pragma unroll
+      for (int j = 0; j < EPT; ++j) sk[tid * EPT + j] = v[j];
+      __syncthreads();
+      for (; stride >= 32 * EPT; stride >>= 1) {
+        for (int t = tid; t < N / 2; t += NT) {
+          const int i = ((t & ~(stride - 1)) << 1) | (t & (stride - 1)), j = i | stride;
           const unsigned long long a = sk[i], b = sk[j];
           const bool desc = (i & size) == 0;
           if (desc ? a < b : a > b) { sk[i] = b; sk[j] = a; }
         }
+        __syncthreads();
       }
-      __syncthreads();
+#pragma unroll
+      for (int j = 0; j < EPT; ++j) v[j] = sk[tid * EPT + j];
+    }
+    for (; stride >= EPT; stride >>= 1) {
+      const int lm = stride / EPT;
+#pragma unroll
+      for (int j = 0; j < EPT; ++j) {
+        const int i = tid * EPT + j;
+        const unsigned long long o = __shfl_xor_sync(0xffffffffu, v[j], lm);
+        const bool hi = ((i & stride) == 0) == ((i & size) == 0);
+        v[j] = hi ? (v[j] > o ? v[j] : o) : (v[j] < o ? v[j] : o);
+      }
+    }
+#pragma unroll
+    for (int s = EPT >> 1; s > 0; s >>= 1) {
+      if (s < size) {
+#pragma unroll
+        for (int j = 0; j < EPT; ++j) {
+          if ((j & s) == 0) {
+            const bool desc = ((tid * EPT + j) & size) == 0;
+            const unsigned long long a = v[j], b = v[j | s];
+            if (desc ? a < b : a > b) { v[j] = b; v[j | s] = a; }
+          }
+        }
+      }
     }
   }
-  const int k = (int)min((int64_t)W, k_c[r]);
-  const double p = p_c[r];
-  uint32_t L = (uint32_t)k;
-  if (p < 1.0) {
+  __syncthreads();  // the last shared-memory phase's readers are done
+#pragma unroll
+  for (int j = 0; j < EPT; ++j) sk[tid * EPT + j] = v[j];
+  __syncthreads();
+}
+
+// NT threads sort NT * EPT >= W entries; the mass scan runs on the first kThreads of them.
+template <int NT, int EPT>
+__global__ void __launch_bounds__(NT) tp_small_resolve(const uint32_t *recv, size_t send_words, int B4, int B,
+                                                          int kmax, int world, const int64_t *kk,
+                                                          const double *pp, TpRow *rows, int32_t *kidx_c,
+                                                          int32_t *kc_c, int W) {
+  extern __shared__ unsigned long long sk[];  // [NT * EPT]
+  constexpr int Wp = NT * EPT;
+  __shared__ Fx scan_buf[kWarps];
+  __shared__ uint32_t s_L, s_keep;
+  const int r = blockIdx.x, tid = threadIdx.x;
+  const int mode = rows[r].mode;
+  if (mode != MODE_TOPK && mode != MODE_TOPKP) {
+    // top-p-only rows: each shard sent one candidate, its max (tp_merge's rule)
+    if (mode == MODE_TOPP && tid == 0) {
+      uint32_t mk = 0u;
+      for (int g = 0; g < world; ++g) {
+        const uint32_t *sg = recv + (size_t)g * send_words;
+        if (sg[r]) mk = max(mk, sg[B4 + (size_t)r * kmax]);
+      }
+      rows[r].maxkey = mk;
+    }
+    return;
+  }
+  // the ranks' candidate lists straight from the all-gather buffer, as (key, ~global column)
+  // composites; pads (0) sort after every real entry
+  for (int i = tid; i < Wp; i += NT) sk[i] = 0ull;
+  __syncthreads();
+  uint32_t n = 0u;
+  for (int g = 0; g < world; ++g) {
+    const uint32_t *sg = recv + (size_t)g * send_words;
+    const uint32_t ng = sg[r];
+    const uint32_t *keys = sg + B4 + (size_t)r * kmax;
+    const uint32_t *gid = sg + B4 + (size_t)B * kmax + (size_t)r * kmax;
+    for (uint32_t i = tid; i < ng; i += NT) sk[n + i] = ((unsigned long long)keys[i] << 32) | (0xffffffffu - gid[i]);
+    n += ng;
+  }
+  __syncthreads();
+  bitonic_desc<NT, EPT>(sk);
+  const int k = (int)min((int64_t)n, kk[r]);
+  const double p = pp[r];
+  if (tid == 0) s_keep = (uint32_t)k;
+  if (p < 1.0 && tid < kThreads) {
     const double m = value_of_key((uint32_t)(sk[0] >> 32));
-    const int E = (k + kT - 1) / kT, q0 = tid * E;
+    const int E = (k + kThreads - 1) / kThreads, q0 = tid * E;
     Fx d = fx_zero();
     for (int j = 0; j < E; ++j)
       if (q0 + j < k) d = fx_add(d, fx_from_double(exp(value_of_key((uint32_t)(sk[q0 + j] >> 32)) - m)));
@@ -580,10 +662,12 @@ __global__ void __launch_bounds__(kT) tp_small_resolve(const float *cval, int W,
       }
     }
     tsync();
-    L = fx_ge(total, fx_round_threshold(nextafter(p, 2.0))) ? s_L : (uint32_t)k;  // oracle.py:44-46
+    if (tid == 0 && fx_ge(total, fx_round_threshold(nextafter(p, 2.0)))) s_keep = s_L;  // oracle.py:44-46
   }
-  for (int i = tid; i < (int)L; i += kT) kidx_c[(size_t)r * W + i] = (int32_t)(0xffffffffu - (uint32_t)sk[i]);
-  if (tid == 0) kc_c[r] = (int32_t)L;
+  __syncthreads();
+  const int L = (int)s_keep;
+  for (int i = tid; i < L; i += NT) kidx_c[(size_t)r * W + i] = (int32_t)(0xffffffffu - (uint32_t)sk[i]);
+  if (tid == 0) kc_c[r] = L;
 }
 
 // ------------------------------------------------------------------------------------------------
@@ -688,6 +772,17 @@ cudaError_t smem_optin(K kernel, int *slots) {
   }, v);
 }
 
+template <int NT, int EPT>
+cudaError_t launch_small(const uint32_t *recv, const TpLayout &L, int B, int world, const int64_t *k, const double *p,
+                         TpRow *rows, int32_t *kidx_c, int32_t *kc_c, cudaStream_t st) {
+  constexpr size_t sbytes = (size_t)NT * EPT * 8;
+  static int optin[kMaxDevices] = {};
+  if (sbytes > (48u << 10) && smem_optin(tp_small_resolve<NT, EPT>, optin) != cudaSuccess) return cudaErrorUnknown;
+  tp_small_resolve<NT, EPT><<<B, NT, sbytes, st>>>(recv, L.send_words, L.B4, B, L.kmax, world, k, p, rows, kidx_c,
+                                                   kc_c, L.W);
+  return cudaGetLastError();
+}
+
 template <typename T>
 int run_tp(const void *logits, int64_t ld_in, int dtype, int B, int Vr, int Vg, int64_t offset, const int64_t *k,
            const double *p, int k_cap, void *out, int64_t ld_out, int32_t *kept_count, void *workspace,
@@ -705,6 +800,7 @@ int run_tp(const void *logits, int64_t ld_in, int dtype, int B, int Vr, int Vg, 
       return QRITA_ECUDA;
   }
   const T *x = (const T *)logits;
+  const bool small = L.W <= kSmallW;  // candidate rows resolved by tp_small_resolve
   int64_t *k_loc = (int64_t *)at(L.k_loc), *k_c = (int64_t *)at(L.k_c);
   double *p_one = (double *)at(L.p_one), *p_c = (double *)at(L.p_c);
   TpRow *rows = (TpRow *)at(L.rows);
@@ -721,26 +817,32 @@ int run_tp(const void *logits, int64_t ld_in, int dtype, int B, int Vr, int Vg, 
                           (int32_t *)at(L.kc_s), nullptr, at(L.ws0), L.ws0_bytes, 0, 4096, (qrita_stream_t)st,
                           nullptr, nullptr, nullptr, nullptr, (int32_t *)at(L.kidx_s), L.kmax);
   if (rc != QRITA_OK) return rc;
-  tp_pack<T><<<B, kT, bm_bytes, st>>>(x, ld_in, Vr, offset, L.kmax, (const int32_t *)at(L.kc_s),
-                                      (const int32_t *)at(L.kidx_s), (uint32_t *)at(L.send), L.B4, B);
+  tp_pack<T><<<B, kT, small ? 0 : bm_bytes, st>>>(x, ld_in, Vr, offset, L.kmax, (const int32_t *)at(L.kc_s),
+                                      (const int32_t *)at(L.kidx_s), (uint32_t *)at(L.send), L.B4, B, small ? 0 : 1);
   if (cudaGetLastError() != cudaSuccess) return QRITA_ECUDA;
   if (comm->all_gather(at(L.send), at(L.recv), 4 * L.send_words, (qrita_stream_t)st, comm->ctx) != 0)
     return QRITA_ENCCL;
-  tp_merge<<<B, kT, 0, st>>>((const uint32_t *)at(L.recv), L.send_words, L.B4, B, L.kmax, world, L.W, k, p, rows,
-                             (float *)at(L.cval), (uint32_t *)at(L.cgid), k_c, p_c);
-  if (cudaGetLastError() != cudaSuccess) return QRITA_ECUDA;
   // (2) the exact answer on the gathered candidates (same on every rank): a shared-memory sort for
   //     candidate rows up to kSmallW entries, else the single-GPU kernels
-  if (L.W <= kSmallW) {
-    int wp = 1;
-    while (wp < L.W) wp <<= 1;
-    const size_t sbytes = (size_t)wp * 8;
-    static int optin_small[kMaxDevices] = {};
-    if (sbytes > (48u << 10) && smem_optin(tp_small_resolve, optin_small) != cudaSuccess) return QRITA_ECUDA;
-    tp_small_resolve<<<B, kT, sbytes, st>>>((const float *)at(L.cval), L.W, wp, k_c, p_c, (int32_t *)at(L.kidx_c),
-                                            (int32_t *)at(L.kc_c));
-    if (cudaGetLastError() != cudaSuccess) return QRITA_ECUDA;
+  if (small) {
+    const uint32_t *recv = (const uint32_t *)at(L.recv);
+    int32_t *kidx_c = (int32_t *)at(L.kidx_c), *kc_c = (int32_t *)at(L.kc_c);
+    cudaError_t e;
+    if (L.W <= 1024)
+      e = launch_small<256, 4>(recv, L, B, world, k, p, rows, kidx_c, kc_c, st);
+    else if (L.W <= 2048)
+      e = launch_small<256, 8>(recv, L, B, world, k, p, rows, kidx_c, kc_c, st);
+    else if (L.W <= 4096)
+      e = launch_small<256, 16>(recv, L, B, world, k, p, rows, kidx_c, kc_c, st);
+    else if (L.W <= 8192)
+      e = launch_small<512, 16>(recv, L, B, world, k, p, rows, kidx_c, kc_c, st);
+    else
+      e = launch_small<1024, 16>(recv, L, B, world, k, p, rows, kidx_c, kc_c, st);
+    if (e != cudaSuccess) return QRITA_ECUDA;
   } else {
+    tp_merge<<<B, kT, 0, st>>>((const uint32_t *)at(L.recv), L.send_words, L.B4, B, L.kmax, world, L.W, k, p, rows,
+                               (float *)at(L.cval), (uint32_t *)at(L.cgid), k_c, p_c);
+    if (cudaGetLastError() != cudaSuccess) return QRITA_ECUDA;
     rc = topk_topp_impl(at(L.cval), L.W, QRITA_DTYPE_F32, B, L.W, k_c, p_c, nullptr, L.W, (int32_t *)at(L.kc_c),
                         nullptr, at(L.ws1), L.ws1_bytes, 0, 4096, (qrita_stream_t)st, nullptr, nullptr, nullptr,
                         nullptr, (int32_t *)at(L.kidx_c), L.W);
@@ -766,7 +868,8 @@ int run_tp(const void *logits, int64_t ld_in, int dtype, int B, int Vr, int Vg, 
   }
   // (4) the shard output
   const WsLayout W0 = ws_layout(B, Vr);
-  tp_write<T><<<B, kT, bm_bytes, st>>>(x, ld_in, (T *)out, ld_out, Vr, offset, rows, (const uint32_t *)at(L.cgid),
+  tp_write<T><<<B, kT, bm_bytes, st>>>(x, ld_in, (T *)out, ld_out, Vr, offset, rows,
+                                       small ? nullptr : (const uint32_t *)at(L.cgid),
                                        (const int32_t *)at(L.kidx_c), (const int32_t *)at(L.kc_c), L.W,
                                        (const uint32_t *)at(L.qbuf), rank, world, kept_count,
                                        (int32_t *)(ws + L.ws0 + W0.status), tst, sh, bg ? 1 : 0,

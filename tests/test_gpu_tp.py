@@ -66,6 +66,22 @@ def test_mixed_rows_vs_oracle(cuda_device, world, dtype):
     assert np.array_equal(kc.cpu().numpy(), (~np.isneginf(want)).sum(1))
 
 
+@pytest.mark.parametrize("world", [16, 20])
+def test_wide_candidate_rows(cuda_device, world):
+    """world * k_cap candidates per row: 16 x 1000 takes the widest shared-memory sort (16384 slots),
+    20 x 1000 the single-GPU kernels on column-ordered candidate rows."""
+    rng = np.random.default_rng(77 + world)
+    b, v = 6, 24000
+    x = rng.normal(0, 1, (b, v)).astype(np.float32)
+    x[3:] = np.round(x[3:] * 8) / 8                   # ties across shards
+    k = np.array([1000, 999, 640, 1000, 17, 1000], dtype=np.int64)
+    p = np.array([0.9, 1.0, 0.5, 0.999, 0.7, 1.0])
+    want, _ = oracle_batch(x, k, p)
+    out = simulate_tp(torch.from_numpy(x).cuda(), torch.from_numpy(k).cuda(), torch.from_numpy(p).cuda(),
+                      world=world)
+    _check(x, out.cpu().numpy(), want, f"wide world={world}")
+
+
 def test_cfg3_rows_topp_only_bf16_tp4(cuda_device):
     x, k, p, _, trip, _ = G.config("cfg3")
     rows = slice(0, 8)
