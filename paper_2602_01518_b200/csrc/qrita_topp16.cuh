@@ -27,9 +27,6 @@
 
 #include "qrita_plan.cuh"
 
-#ifndef QRITA_T16_MATCH  // warp-aggregate equal values in the count pass (match.any)
-#define QRITA_T16_MATCH 0
-#endif
 
 namespace qrita {
 
@@ -60,7 +57,6 @@ struct T16Shared {
   uint32_t kq;                   // entries kept in this CTA's segment
   uint32_t pres[kSteps16 / 32];  // steps (32 consecutive u) with a value in this CTA's segment
   uint32_t nsteps, xstep;        // present steps of this CTA's u range; the step holding the crossing
-  uint32_t total16;              // sum of this CTA's counters (16-bit wrap check)
 };
 
 __device__ __forceinline__ uint32_t u_full_key(uint32_t u) {
@@ -97,8 +93,17 @@ __device__ __forceinline__ void t16_stamp(const Params &P, int row, uint32_t q, 
 // ("steps") of h and of u correspond.  -0.0 (h = 0x8000) ranks with +0.0 (u = 0x8000).
 __device__ __forceinline__ uint32_t h_of_u(uint32_t u) { return u >= 0x8000u ? (u ^ 0x8000u) : (u ^ 0xffffu); }
 __device__ __forceinline__ uint32_t u_of_h(uint32_t h) { return h < 0x8000u ? (h | 0x8000u) : (h ^ 0xffffu); }
+// Counter slot of pattern h: the low 5 bits are XOR-ed with the next 5, a bijection inside every
+// 32-pattern step that spreads values with zero low mantissa bits (quantised logits: 0.25, 0.5, ...)
+// over the shared-memory banks instead of piling them onto bank 0.
+__device__ __forceinline__ uint32_t hidx(uint32_t h) { return h ^ ((h >> 5) & 31u); }
 __device__ __forceinline__ uint32_t cnt16(const uint32_t *hw, uint32_t h) {
-  return (hw[h >> 1] >> ((h & 1u) << 4)) & 0xffffu;
+  const uint32_t x = hidx(h);
+  return (hw[x >> 1] >> ((x & 1u) << 4)) & 0xffffu;
+}
+__device__ __forceinline__ void hist_add(uint32_t *hw, uint32_t h, uint32_t c) {
+  const uint32_t x = hidx(h);
+  atomicAdd(&hw[x >> 1], c << ((x & 1u) << 4));  // result unused: red
 }
 // copies of value u counted in one CTA's counters
 __device__ __forceinline__ uint32_t count_u(const uint32_t *hw, uint32_t u) {
@@ -154,13 +159,14 @@ static __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT16, 1) qrit
     s.pl.has_thr = 0;
   }
 
-  // (1) count pass: warp w takes the 256-element chunks w, w + 32, ... of the segment, one 16-byte
-  //     load per lane, the next chunk's load in flight while the current one is counted
+  // (1) count pass: warp w takes the contiguous piece [lo + w * piece, ...) of the segment (the output
+  //     pass's partition) in 256-element steps, one 16-byte load per lane, kD steps in flight
+  const int seg = hi - lo;
+  const int piece = (((seg + kW16 - 1) / kW16) + 255) & ~255;  // per warp, a multiple of 256
+  const int w0 = lo + warp * piece, w1 = min(hi, w0 + piece);
   {
-    const int nchunk = (hi - lo + 255) / 256;
-    auto load = [&](int c, uint4 &w, int &e0, int &n) {
-      e0 = lo + c * 256 + lane * 8;
-      n = c < nchunk ? max(0, min(8, hi - e0)) : 0;
+    auto load = [&](int e0, uint4 &w) -> int {
+      const int n = max(0, min(8, w1 - e0));
       if (vec && n == 8) {
         w = *reinterpret_cast<const uint4 *>(in + e0);
       } else {
@@ -168,23 +174,30 @@ static __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT16, 1) qrit
         for (int j = 0; j < n; ++j) t[j >> 1] |= ((uint32_t)in[e0 + j]) << ((j & 1) << 4);
         w = make_uint4(t[0], t[1], t[2], t[3]);
       }
+      return n;
     };
-    auto add = [&](uint32_t h) { atomicAdd(&hist[h >> 1], 1u << ((h & 1u) << 4)); };  // result unused: red
-    uint4 cur, nxt;
-    int ce0, cn, ne0, nn;
-    load(warp, cur, ce0, cn);
-    for (int c = warp; c < nchunk; c += kW16) {
-      load(c + kW16, nxt, ne0, nn);
-      const uint32_t w4[4] = {cur.x, cur.y, cur.z, cur.w};
-      if (cn == 8) {
+    auto count8 = [&](const uint4 &c, int n) {
+      const uint32_t w4[4] = {c.x, c.y, c.z, c.w};
+      if (n == 8) {
 #pragma unroll
-        for (int j = 0; j < 4; ++j) { add(w4[j] & 0xffffu); add(w4[j] >> 16); }
+        for (int j = 0; j < 4; ++j) { hist_add(hist, w4[j] & 0xffffu, 1u); hist_add(hist, w4[j] >> 16, 1u); }
       } else {
-        for (int j = 0; j < cn; ++j) add((w4[j >> 1] >> ((j & 1) << 4)) & 0xffffu);
+        for (int j = 0; j < n; ++j) hist_add(hist, (w4[j >> 1] >> ((j & 1) << 4)) & 0xffffu, 1u);
       }
-      cur = nxt;
-      ce0 = ne0;
-      cn = nn;
+    };
+    constexpr int kD = 4;
+    uint4 buf[kD];
+    int nb[kD];
+#pragma unroll
+    for (int d = 0; d < kD; ++d) nb[d] = load(w0 + 256 * d + lane * 8, buf[d]);
+    for (int e = w0 + lane * 8; e < w1 + lane * 8; e += 256 * kD) {
+#pragma unroll
+      for (int d = 0; d < kD; ++d) {
+        const uint4 c = buf[d];
+        const int n = nb[d];
+        nb[d] = load(e + 256 * (d + kD), buf[d]);
+        count8(c, n);
+      }
     }
   }
   __syncthreads();  // every count is in
@@ -448,8 +461,8 @@ static __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT16, 1) qrit
       for (int j = 0; j < 32; ++j) {
         const uint32_t h = hw[j];
         if (h) {
-          const uint32_t h0 = (uint32_t)(tid * 64 + 2 * j);
-          kc += (u_of_h(h0) > b ? (h & 0xffffu) : 0u) + (u_of_h(h0 + 1u) > b ? (h >> 16) : 0u);
+          const uint32_t x0 = (uint32_t)(tid * 64 + 2 * j);  // counter slots -> patterns (hidx is an involution)
+          kc += (u_of_h(hidx(x0)) > b ? (h & 0xffffu) : 0u) + (u_of_h(hidx(x0 + 1u)) > b ? (h >> 16) : 0u);
         }
       }
       if (tid == 0) kc += quota;
@@ -471,6 +484,7 @@ static __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT16, 1) qrit
     kbase = q == 0 ? 0u : k_peer;
   }
   t16_stamp(P, row, q, 5);
+  t16_stamp(P, row, q ^ 1u, 12);  // CTA 1's output start / end
   // no distributed shared memory access after this point: arrive now, wait before exiting
   asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
 
@@ -481,9 +495,6 @@ static __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT16, 1) qrit
   uint16_t *out = P.out ? (uint16_t *)P.out + (size_t)row * P.ld_out : nullptr;
   const bool ovec = vec && out && (((uintptr_t)out) & 15u) == 0;
   const bool need_ord = !keep_all && quota > 0u && quota < c_mine;
-  const int seg = hi - lo;
-  const int piece = (((seg + kW16 - 1) / kW16) + 255) & ~255;  // per warp, a multiple of 256
-  const int w0 = lo + warp * piece, w1 = min(hi, w0 + piece);
   const uint32_t bh = keep_all ? 0xff7fu : h_of_u(b);  // keep-all: compare against -max (all are >)
   const __nv_bfloat162 vb2 = __halves2bfloat162(__ushort_as_bfloat16((unsigned short)bh),
                                                 __ushort_as_bfloat16((unsigned short)bh));
@@ -514,16 +525,25 @@ static __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT16, 1) qrit
     gt &= valid;
     eq &= valid;
   };
+  constexpr int kU16 = 4;  // 256-element steps per iteration: four 16-byte loads in flight per lane
   uint32_t ord = 0u, krank = kbase;  // this warp's first b-copy ordinal / kept rank
   if (need_ord || kidx) {
     uint32_t ne = 0u, nk = 0u;
-    for (int e = w0 + lane * 8; e < w1; e += 256) {
-      uint4 w;
-      const int n = load(e, w);
-      uint32_t gt, eq;
-      classify(w, n, gt, eq);
-      ne += (uint32_t)__popc(eq);
-      nk += (uint32_t)__popc(gt);
+    for (int e = w0 + lane * 8; e < w1 + lane * 8; e += 256 * kU16) {
+      uint4 wv[kU16];
+      int nv[kU16];
+#pragma unroll
+      for (int u = 0; u < kU16; ++u) {
+        wv[u] = make_uint4(0u, 0u, 0u, 0u);
+        nv[u] = e + 256 * u < w1 ? load(e + 256 * u, wv[u]) : 0;
+      }
+#pragma unroll
+      for (int u = 0; u < kU16; ++u) {
+        uint32_t gt, eq;
+        classify(wv[u], nv[u], gt, eq);
+        ne += (uint32_t)__popc(eq);
+        nk += (uint32_t)__popc(gt);
+      }
     }
     ne = __reduce_add_sync(0xffffffffu, ne);
     nk = __reduce_add_sync(0xffffffffu, nk);
@@ -591,7 +611,6 @@ static __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT16, 1) qrit
       for (uint32_t mm = keepm; mm; mm &= mm - 1u) kidx[pos++] = e + __ffs(mm) - 1;
     }
   };
-  constexpr int kU16 = 4;  // 256-element steps per iteration: four 16-byte loads in flight per lane
   for (int e = w0 + lane * 8; e < w1 + lane * 8; e += 256 * kU16) {
     uint4 wv[kU16];
     int nv[kU16];
@@ -611,6 +630,7 @@ static __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT16, 1) qrit
     }
   }
   t16_stamp(P, row, q, 6);
+  t16_stamp(P, row, q ^ 1u, 13);
   asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
