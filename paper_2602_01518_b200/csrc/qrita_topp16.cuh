@@ -539,10 +539,19 @@ static __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT16, 1) qrit
       }
 #pragma unroll
       for (int u = 0; u < kU16; ++u) {
-        uint32_t gt, eq;
-        classify(wv[u], nv[u], gt, eq);
-        ne += (uint32_t)__popc(eq);
-        nk += (uint32_t)__popc(gt);
+        if (!kidx && nv[u] == 8) {  // copies of b only: 16-bit lane masks
+          const uint32_t x[4] = {wv[u].x, wv[u].y, wv[u].z, wv[u].w};
+          uint32_t c = 0u;
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            c += (uint32_t)__popc(__heq2_mask(*reinterpret_cast<const __nv_bfloat162 *>(&x[j]), vb2));
+          ne += c >> 4;
+        } else {
+          uint32_t gt, eq;
+          classify(wv[u], nv[u], gt, eq);
+          ne += (uint32_t)__popc(eq);
+          nk += (uint32_t)__popc(gt);
+        }
       }
     }
     ne = __reduce_add_sync(0xffffffffu, ne);
@@ -611,6 +620,69 @@ static __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT16, 1) qrit
       for (uint32_t mm = keepm; mm; mm &= mm - 1u) kidx[pos++] = e + __ffs(mm) - 1;
     }
   };
+  // fast path (no kept-column list, full 16-byte vectors): 16-bit lane masks straight from the bf16
+  // pair compares, the output word in one LOP3; copies of b are ranked only in the one 256-element
+  // step of the warp where the quota runs out
+  const bool fast = ovec && !kidx;
+  auto emit_vec = [&](int e, const uint4 &w) {
+    const uint32_t x[4] = {w.x, w.y, w.z, w.w};
+    uint32_t gm[4], em[4], km[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const __nv_bfloat162 v2 = *reinterpret_cast<const __nv_bfloat162 *>(&x[j]);
+      gm[j] = __hgt2_mask(v2, vb2);
+      em[j] = __heq2_mask(v2, vb2);
+    }
+    if (keep_all) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) km[j] = 0xffffffffu;
+    } else if (!need_ord) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) km[j] = gm[j] | (quota > 0u ? em[j] : 0u);
+    } else {
+      uint32_t ne = 0u;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) ne += (uint32_t)__popc(em[j]);
+      ne >>= 4;
+      const uint32_t tot = __reduce_add_sync(0xffffffffu, ne);
+      uint32_t r;  // copies of b this lane keeps
+      if (ord + tot <= quota) {
+        r = ne;
+      } else if (ord >= quota) {
+        r = 0u;
+      } else {
+        uint32_t incl = ne;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += t;
+        }
+        const uint32_t my = ord + incl - ne;
+        r = quota > my ? min(quota - my, ne) : 0u;
+      }
+      ord += tot;
+      uint32_t left = r;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        uint32_t k = gm[j];
+        if (r == ne) {
+          k |= em[j];
+        } else if (left) {  // the lane holding the quota's end: its first `left` copies
+          if ((em[j] & 0xffffu) && left) { k |= 0xffffu; --left; }
+          if ((em[j] & 0xffff0000u) && left) { k |= 0xffff0000u; --left; }
+        }
+        km[j] = k;
+      }
+    }
+    uint32_t kc = 0u, o4[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      kc += (uint32_t)__popc(km[j]);
+      o4[j] = (x[j] & km[j]) | (0xff80ff80u & ~km[j]);
+    }
+    nkept += kc >> 4;
+    __stcs(reinterpret_cast<uint4 *>(out + e), make_uint4(o4[0], o4[1], o4[2], o4[3]));
+  };
   for (int e = w0 + lane * 8; e < w1 + lane * 8; e += 256 * kU16) {
     uint4 wv[kU16];
     int nv[kU16];
@@ -620,7 +692,10 @@ static __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT16, 1) qrit
       nv[u] = e + 256 * u < w1 ? load(e + 256 * u, wv[u]) : 0;
     }
 #pragma unroll
-    for (int u = 0; u < kU16; ++u) emit(e + 256 * u, wv[u], nv[u]);
+    for (int u = 0; u < kU16; ++u) {
+      if (fast && __all_sync(0xffffffffu, nv[u] == 8)) emit_vec(e + 256 * u, wv[u]);
+      else emit(e + 256 * u, wv[u], nv[u]);
+    }
   }
   if (!kidx) {  // kept counts: both CTAs add theirs (zeroed by CTA 0 before barrier #4)
     nkept = __reduce_add_sync(0xffffffffu, nkept);
