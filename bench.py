@@ -515,8 +515,13 @@ def bench_tp(args, rank: int, world: int, dev):
     def call():
         topk_topp_tp(shard, k, p, vocab_offset=bounds[rank], vocab_size=v, comm=comm, k_cap=kcap, out=out,
                      topp_only_rows=False)
-    for _ in range(args.warmup):
+    flush_sink = torch.empty(1, dtype=torch.float32, device=dev)
+
+    def l2_flush():  # as in the single-GPU arm: write 256 MB, read it back (clean eviction)
         flush.zero_()
+        torch.sum(flush, dim=0, keepdim=True, out=flush_sink)
+    for _ in range(args.warmup):
+        l2_flush()
         call()
     torch.cuda.synchronize(dev)
     if world > 1:
@@ -524,7 +529,7 @@ def bench_tp(args, rank: int, world: int, dev):
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(args.steps)]
     with ClockSampler(dev.index) as clk:
         for e0, e1 in evs:
-            flush.zero_()
+            l2_flush()
             if world > 1:
                 dist.barrier()   # synchronised start of every step
             e0.record(st)
@@ -542,7 +547,7 @@ def bench_tp(args, rank: int, world: int, dev):
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": f"cfg5: vocab-sharded TP={world}, B=128 x V=262144 fp32, k~U{{1..1024}}, "
                                f"p~U[0.5,0.99]; shard [128, {bounds[1] - bounds[0]}] per rank",
-                   "batch": b, "vocab": v, "l2": "flushed between steps",
+                   "batch": b, "vocab": v, "l2": "flushed between steps (256 MB write + read-back, untimed)",
                    "parallelism": f"tp{world} (vocab shards, NCCL partials)"},
         "roofline": {"bound": "hbm", "achieved": alg / (ms / 1e3) / 1e9, "peak": peak, "unit": "GB/s",
                      "frac": alg / (ms / 1e3) / 1e9 / peak, "traffic": None, "peak_source": peak_kind,
@@ -550,7 +555,7 @@ def bench_tp(args, rank: int, world: int, dev):
                      "alg_bytes_per_launch": alg},
         "exchange_bytes_per_row_per_rank": 8 * kmax + 4,
         "clocks": clk.summary(),
-        "gpu_launches": 6 * args.steps,
+        "gpu_launches": 5 * args.steps,  # prep, local fused, pack, small resolve, write (+ NCCL all-gather)
     }
     comm.close()
     if world > 1:

@@ -28,6 +28,10 @@
 #include "qrita_plan.cuh"
 
 
+#ifndef QRITA_T16_KD  // 256-element steps of the count pass in flight per warp
+#define QRITA_T16_KD 4
+#endif
+
 namespace qrita {
 
 namespace cg = cooperative_groups;
@@ -185,7 +189,7 @@ static __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT16, 1) qrit
         for (int j = 0; j < n; ++j) hist_add(hist, (w4[j >> 1] >> ((j & 1) << 4)) & 0xffffu, 1u);
       }
     };
-    constexpr int kD = 4;
+    constexpr int kD = QRITA_T16_KD;
     uint4 buf[kD];
     int nb[kD];
 #pragma unroll
