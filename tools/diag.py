@@ -267,7 +267,7 @@ if len(sys.argv) > 1 and sys.argv[1] == "t16timing":
     t0 = a[:, 0].min()
     print(f"cfg3 topp16: start spread {(a[:,0].max()-t0)/1e3:.1f} us, last end {(a[:,6].max()-t0)/1e3:.1f} us")
     for nm, i, j in (("count", 0, 1), ("sync1", 1, 2), ("merge+D", 2, 3), ("mass", 3, 7), ("suffix", 7, 8),
-                     ("sync3", 8, 9), ("xfind", 9, 10), ("xwarp+s4", 10, 4), ("keptloop", 4, 11), ("kept", 11, 5),
+                     ("sync3", 8, 9), ("xfind", 9, 10), ("xwarp+s4", 10, 4), ("kept", 4, 5),
                      ("output", 5, 6), ("out(cta1)", 12, 13)):
         d = (a[:, j] - a[:, i]) / 1e3
         print(f"   {nm:10s} mean {d.mean():7.2f} us  min {d.min():7.2f}  max {d.max():7.2f}")

@@ -3,8 +3,9 @@
 # bench values.  Summarise with: python tools/summarize_profiles.py <tag>
 mkdir -p gpurun_out/prof
 for c in cfg2 cfg4 cfg3 cfg1 cfg5 cfg2copy; do
+  # cfg5: the TP kernels (qrita::tp::tp_*) next to the shard's qrita_fused
   ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
-      -k regex:qrita -s 3 -c 12 --csv --log-file gpurun_out/prof/launches_$c.csv \
+      -k "regex:qrita|tp_" -s 3 -c 12 --csv --log-file gpurun_out/prof/launches_$c.csv \
       python bench.py --config $c --steps 3 --warmup 3 --no-extras > /dev/null 2>&1
 done
 ncu --set full --clock-control none --import-source on -k regex:qrita_fused -s 3 -c 1 \
