@@ -229,6 +229,25 @@ int qrita_sigma_table(int kind, double *out, int n);
 int qrita_row_stats(const void *logits, int64_t ld, int dtype, int B, int V, int sample_size, double *out,
                     qrita_stream_t stream);
 
+/* LM-head producer fusion (the reference has no code for this producer — its
+ * consumer is truncate_topk_topp, pipeline.py:199-239, ground truth oracle.py:70-89):
+ *   logits[b][v] = sum_k hidden[b][k] * weight[v][k]  — hidden [B, d] and weight [V, d] bf16 row-major
+ *   (leading dimensions ld_h / ld_w elements, 16-byte aligned), d % 64 == 0, fp32 accumulation on the
+ *   tensor cores (tcgen05.mma, TMA-fed), logits fp32 [B, ld_logits].
+ *   qrita_lmhead_logits      the plain GEMM (also the reference the fused call is checked against).
+ *   qrita_lmhead_topk_topp   the GEMM with the truncation's streaming pass in its epilogue: writes the
+ *                            logits once and the exact Top-k/Top-p kept columns (kept_idx [B][ld_idx],
+ *                            unordered) and counts — identical to qrita_topk_topp_idx on those logits;
+ *                            on a sigma hit the logits are never read back.  Workspace:
+ *                            qrita_lmhead_workspace_bytes(B, V); status via qrita_get_status(workspace). */
+int qrita_lmhead_logits(const void *hidden, int64_t ld_h, const void *weight, int64_t ld_w, int B, int V, int d,
+                        float *logits, int64_t ld_logits, qrita_stream_t stream);
+size_t qrita_lmhead_workspace_bytes(int B, int V);
+int qrita_lmhead_topk_topp(const void *hidden, int64_t ld_h, const void *weight, int64_t ld_w, int B, int V, int d,
+                           const int64_t *k, const double *p, float *logits, int64_t ld_logits, int32_t *kept_idx,
+                           int64_t ld_idx, int32_t *kept_count, qrita_row_metrics *metrics, void *workspace,
+                           size_t ws_bytes, int flags, qrita_stream_t stream);
+
 /* Synchronises `stream`, then reports the first failing row of the last call on this workspace:
  * returns QRITA_OK or QRITA_EINVAL_K / QRITA_EINVAL_P / QRITA_ENONFINITE, and fills *row / *col
  * (col = first non-finite column, or -1). */

@@ -19,7 +19,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
               "-I" + os.path.join(ROOT, "include"), "-I" + CSRC]
 
-SOURCES = ["qrita_capi.cu", "qrita_f32.cu", "qrita_bf16.cu", "qrita_tp.cu", "qrita_prims.cu"]
+SOURCES = ["qrita_capi.cu", "qrita_f32.cu", "qrita_bf16.cu", "qrita_tp.cu", "qrita_prims.cu", "qrita_lmhead.cu"]
 
 
 def _nvcc() -> str:

@@ -267,6 +267,9 @@ int qrita_topk_topp(const void *logits, int64_t ld_in, int dtype, int B, int V,
 
 namespace qrita {
 
+// numpy's pairwise-sum tree over the first n elements (the sigma plan's sample), for other TUs
+void pw_tree_build(int n, PwTree &t) { pw_tree(n, t); }
+
 // qrita_topk_topp_ex with the status / nf_col words optionally placed outside the workspace (the
 // host-buffer pipeline gathers the chunks' status into one [B] block).
 int topk_topp_impl(const void *logits, int64_t ld_in, int dtype, int B, int V, const int64_t *k, const double *p,

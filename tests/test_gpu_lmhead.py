@@ -1,0 +1,79 @@
+"""GPU: the LM-head producer fusion (csrc/qrita_lmhead.cu).  The tcgen05 GEMM is checked against a
+torch fp32 matmul of the same bf16 operands (tolerance below: fp32 accumulation order differs), the
+fused call's logits against the plain GEMM bit for bit, and its kept sets against
+topk_topp_indices on those logits and the oracle (oracle.py:70-89) — bit-exact."""
+import numpy as np
+import pytest
+import torch
+
+import paper_2602_01518_b200 as Q
+from oracle.qrita_oracle import oracle_batch
+from paper_2602_01518_b200.lmhead import lm_head_logits, lm_head_topk_topp
+
+pytestmark = pytest.mark.gpu
+
+
+def _operands(b, v, d, seed):
+    g = torch.Generator(device="cpu").manual_seed(seed)
+    h = torch.randn(b, d, generator=g).to(torch.bfloat16).cuda()
+    w = (torch.randn(v, d, generator=g) / d ** 0.5).to(torch.bfloat16).cuda()
+    return h, w
+
+
+@pytest.mark.parametrize("b,v,d", [(1, 1000, 64), (8, 4096, 128), (37, 5000, 256), (256, 32000, 512),
+                                   (300, 2100, 192)])
+def test_logits_match_fp32_matmul(cuda_device, b, v, d):
+    h, w = _operands(b, v, d, b + v + d)
+    got = lm_head_logits(h, w)
+    want = h.float() @ w.float().T
+    scale = (h.float().abs() @ w.float().abs().T)
+    # |fp32 sum reordering| <= d * 2^-24 * sum |terms|; 4x margin
+    tol = 4 * d * 2.0 ** -24 * scale
+    assert bool(((got - want).abs() <= tol + 1e-30).all()), float(((got - want).abs() / (scale + 1e-30)).max())
+
+
+def _kept_sets(idx, cnt):
+    idx, cnt = idx.cpu().numpy(), cnt.cpu().numpy()
+    return [np.sort(idx[r, :cnt[r]]) for r in range(len(cnt))]
+
+
+@pytest.mark.parametrize("b,v,d", [(4, 4096, 128), (37, 32000, 256), (130, 9000, 128), (300, 5000, 64)])
+def test_fused_kept_sets_exact(cuda_device, b, v, d):
+    h, w = _operands(b, v, d, 7 * b + v)
+    if b > 5:
+        h[5] = 0                                        # an all-tied row (every logit 0)
+    rng = np.random.default_rng(b + v)
+    k = rng.integers(1, 1025, b).astype(np.int64)
+    p = rng.uniform(0.3, 0.99, b)
+    k[::7] = v                                          # top-p only (whole row)
+    p[1::5] = 1.0                                       # top-k only
+    if b > 3:
+        k[3], p[3] = v, 1.0                             # pass-through
+    logits, kidx, kc = lm_head_topk_topp(h, w, torch.from_numpy(k), torch.from_numpy(p), check=True)
+    ref = lm_head_logits(h, w)
+    assert torch.equal(logits, ref)
+    want_idx, want_cnt = Q.topk_topp_indices(ref, torch.from_numpy(k).cuda(), torch.from_numpy(p).cuda())
+    got, want = _kept_sets(kidx, kc), _kept_sets(want_idx, want_cnt)
+    assert all(np.array_equal(a, c) for a, c in zip(got, want))
+    masked, _ = oracle_batch(ref.cpu().numpy(), k, p)
+    for r in range(b):
+        assert np.array_equal(got[r], np.nonzero(~np.isneginf(masked[r]))[0]), r
+
+
+def test_fused_forced_fallback_and_binary(cuda_device):
+    h, w = _operands(16, 6000, 128, 11)
+    k = torch.full((16,), 40, dtype=torch.int64)
+    p = torch.full((16,), 0.8, dtype=torch.float64)
+    ref = lm_head_logits(h, w)
+    want = _kept_sets(*Q.topk_topp_indices(ref, k.cuda(), p.cuda()))
+    for fl in (Q.TruncFlags(force_fallback=True), Q.TruncFlags(search="binary"), Q.TruncFlags(use_sigma_trunc=False)):
+        _, kidx, kc = lm_head_topk_topp(h, w, k, p, flags=fl)
+        assert all(np.array_equal(a, c) for a, c in zip(_kept_sets(kidx, kc), want))
+
+
+def test_fused_invalid_rows_raise(cuda_device):
+    h, w = _operands(4, 1000, 64, 2)
+    with pytest.raises(ValueError):
+        lm_head_topk_topp(h, w, torch.tensor([5, 0, 5, 5]), 0.9, check=True)
+    with pytest.raises(ValueError):
+        lm_head_logits(h[:, :60].contiguous(), w[:, :60].contiguous())
