@@ -175,8 +175,9 @@ __device__ __forceinline__ void plan_begin(const Params &P, int row, RowPlan *ou
 }
 
 template <typename T, class SampleAt>
-__device__ void plan_sample(const Params &P, SampleAt xs, const T *a, PlanScratch &sc, RowPlan *out) {
-  const int tid = threadIdx.x;
+__device__ void plan_sample(const Params &P, SampleAt xs, const T *a, PlanScratch &sc, RowPlan *out,
+                            int tid_base = 0) {
+  const int tid = (int)threadIdx.x - tid_base;  // the kThreads-thread group runs from warp tid_base / 32
   if (!out->has_thr) return;  // uniform per group (written before the caller's barrier)
   const PwTree &tr = P.tree;
   const int n = tr.n;
