@@ -213,6 +213,10 @@ def run_reference(args):
     world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
     if rank != 0:
         return
+    if args.config == "lmhead":
+        print(json.dumps({"impl": "reference", "unavailable": "the reference has no LM-head producer "
+                          "(SURVEY.md 8(f) rank 3); compare with this line's unfused_ms instead"}), flush=True)
+        return
     x, k, p, dtype, desc, total_rows, scaling = workload(args.config, 0, 1)
     if args.config == "cfg4":  # the whole 1024-row batch (the CPU path is not sharded over GPUs)
         x, k, p, dtype, desc, total_rows, scaling = workload(args.config, 0, 1)
@@ -294,6 +298,8 @@ def main():
 
     if args.config == "cfg5":
         return bench_tp(args, rank, world, dev)
+    if args.config == "lmhead":
+        return bench_lmhead(args, rank, world, dev)
     x_np, k_np, p_np, dtype, desc, total_rows, scaling = workload(args.config, rank, world)
     tdt = torch.bfloat16 if dtype == "bf16" else torch.float32
     x = torch.from_numpy(x_np).to(dev).to(tdt)
@@ -558,6 +564,101 @@ def bench_tp(args, rank: int, world: int, dev):
         "gpu_launches": 5 * args.steps,  # prep, local fused, pack, small resolve, write (+ NCCL all-gather)
     }
     comm.close()
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
+def bench_lmhead(args, rank: int, world: int, dev):
+    """LM head (Llama-3-8B shape: d=4096, V=128256, B=256 rows per GPU) + exact
+    Top-k/Top-p, fused (qrita_lmhead_topk_topp: tcgen05 GEMM with the streaming pass in its epilogue).
+    Random-init bf16 weights and hidden states; every rank its own replica (weak scaling).  The
+    roofline is the tensor-core one (2*B*V*d flops per call) against the measured bf16 peak; the
+    unfused pipeline (same GEMM, then topk_topp_indices on the logits) is reported beside it."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2602_01518_b200.lmhead import lm_head_logits, lm_head_topk_topp
+    import paper_2602_01518_b200 as Q
+    b, v, d = 256, 128256, 4096
+    g = torch.Generator(device="cpu").manual_seed(17 + rank)
+    h = torch.randn(b, d, generator=g).to(torch.bfloat16).to(dev)
+    w = (torch.randn(v, d, generator=g) / d ** 0.5).to(torch.bfloat16).to(dev)
+    r = np.random.default_rng(2 + rank)
+    k = torch.from_numpy(r.integers(1, 1025, b).astype(np.int64)).to(dev)
+    p = torch.from_numpy(r.uniform(0.5, 0.99, b)).to(dev)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    sink = torch.empty(1, dtype=torch.float32, device=dev)
+    st = torch.cuda.current_stream(dev)
+
+    def l2_flush():
+        flush.zero_()
+        torch.sum(flush, dim=0, keepdim=True, out=sink)
+
+    def timed(fn, steps):
+        for _ in range(2):  # untimed: library handles / first-call setup
+            fn()
+        evs = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(steps)]
+        for e0, e1 in evs:
+            l2_flush()
+            e0.record(st)
+            fn()
+            e1.record(st)
+        torch.cuda.synchronize(dev)
+        return statistics.mean(a.elapsed_time(c) for a, c in evs)
+
+    fused = lambda: lm_head_topk_topp(h, w, k, p)
+    logits = torch.empty(b, v, dtype=torch.float32, device=dev)
+    unfused = lambda: Q.topk_topp_indices(lm_head_logits(h, w, out=logits), k, p)
+    for _ in range(args.warmup):
+        l2_flush()
+        fused()
+        unfused()
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    with ClockSampler(dev.index) as clk:
+        ms = timed(fused, args.steps)
+    ms = sharded_max(ms, world, dev)
+    ms_unfused = sharded_max(timed(unfused, max(3, args.steps // 2)), world, dev)
+    ms_gemm = sharded_max(timed(lambda: lm_head_logits(h, w, out=logits), max(3, args.steps // 2)), world, dev)
+    ms_cublas = sharded_max(timed(lambda: h @ w.T, max(3, args.steps // 2)), world, dev)
+    # end to end: hidden states from pinned host memory in, kept columns + counts back to the host
+    h_host = h.cpu().pin_memory()
+    kidx_host = torch.empty(b, v, dtype=torch.int32).pin_memory()
+    kc_host = torch.empty(b, dtype=torch.int32).pin_memory()
+
+    def e2e():
+        hd = h_host.to(dev, non_blocking=True)
+        _, kidx, kc = lm_head_topk_topp(hd, w, k, p)
+        kidx_host.copy_(kidx, non_blocking=True)
+        kc_host.copy_(kc, non_blocking=True)
+    ms_e2e = sharded_max(timed(e2e, max(3, args.steps // 2)), world, dev)
+    flops = 2.0 * b * v * d
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            peak, kind = float(json.load(fh)["bf16_tflops"]), "measured"
+    except Exception:
+        peak, kind = 2250.0, "fallback (nominal dense bf16)"
+    line = {
+        "metric": "rows/sec for LM head + Top-k+Top-p (fused), B=256, V=128k, d=4096", "value": world * b / (ms / 1e3),
+        "unit": "rows/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16 (fp32 accumulate)",
+        "data": "synthetic (random-init bf16 LM-head weights and hidden states)",
+        "config": {"workload": "lmhead: Llama-3-8B LM head (d=4096, V=128256), B=256 rows per GPU, "
+                               "k~U{1..1024}, p~U[0.5,0.99]", "batch": b, "vocab": v, "hidden": d,
+                   "l2": "flushed between steps (256 MB write + read-back, untimed)"},
+        "roofline": {"bound": "tensor", "achieved": flops / (ms / 1e3) / 1e12, "peak": peak, "unit": "TFLOP/s",
+                     "frac": flops / (ms / 1e3) / 1e12 / peak, "traffic": None, "peak_source": kind,
+                     "kernel": "whole qrita_lmhead_topk_topp call (GEMM + epilogue + row tails)"},
+        "unfused_ms": ms_unfused, "gemm_only_ms": ms_gemm, "cublas_bf16_matmul_ms": ms_cublas,
+        "e2e": {"value": world * b / (ms_e2e / 1e3), "unit": "rows/s", "h2d_bytes_per_step": b * d * 2,
+                "d2h_bytes_per_step": b * v * 4 + b * 4, "ms_per_step": ms_e2e},
+        "clocks": clk.summary(),
+        "gpu_launches": 2 * args.steps,  # lmh_gemm, qrita_tail (plus a counter memset)
+    }
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
