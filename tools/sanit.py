@@ -5,7 +5,8 @@
 Cases: cfg1; cfg2 (first 32 rows); cfg3 (4 rows, bf16, top-p only: distinct-value path); mixed (700
 rows x 5000 with every mode, ties and an all-equal row: several rows per CTA); staged (V = 4999, the
 unaligned 3-kernel pipeline); idx (kept-index output); nodup / binary / fallback ablations; tp
-(the vocab-sharded protocol, 2 ranks as threads); host (the host-buffer pipeline, pageable).
+(the vocab-sharded protocol, 2 ranks as threads); host (the host-buffer pipeline, pageable); lmhead
+(the LM-head GEMM with the fused streaming epilogue, in-kernel plans).
 Each case checks its result against the oracle and prints "ok <case>"."""
 import os
 import sys
@@ -82,6 +83,19 @@ def main(case):
             out = simulate_tp(torch.from_numpy(x).cuda().to(dt), torch.from_numpy(k).cuda(),
                               torch.from_numpy(p).cuda(), world=2)
             check(x, out.float().cpu().numpy(), k, p, f"tp {dt}")
+    elif case == "lmhead":
+        from paper_2602_01518_b200.lmhead import lm_head_topk_topp
+        g = torch.Generator().manual_seed(3)
+        h = torch.randn(16, 128, generator=g).to(torch.bfloat16).cuda()
+        w = (torch.randn(5000, 128, generator=g) / 128 ** 0.5).to(torch.bfloat16).cuda()
+        _, k, p = mixed(16, 5000, 10)
+        logits, idx, cnt = lm_head_topk_topp(h, w, torch.from_numpy(k), torch.from_numpy(p), check=True)
+        x = logits.cpu().numpy()
+        idx, cnt = idx.cpu().numpy(), cnt.cpu().numpy()
+        got = np.full_like(x, -np.inf)
+        for i in range(x.shape[0]):
+            got[i, idx[i, :cnt[i]]] = x[i, idx[i, :cnt[i]]]
+        check(x, got, k, p, case)
     elif case == "host":
         x, k, p = mixed(200, 8192, 9)
         out = Q.topk_topp(torch.from_numpy(x), torch.from_numpy(k), torch.from_numpy(p))
