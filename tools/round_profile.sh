@@ -13,3 +13,9 @@ ncu --set full --clock-control none --import-source on -k regex:qrita_fused -s 3
 ncu --set full --clock-control none --import-source on -k regex:qrita_topp16 -s 3 -c 1 \
     -o gpurun_out/prof/topp16_cfg3 python bench.py --config cfg3 --steps 1 --warmup 3 --no-extras \
     > gpurun_out/prof/topp16_cfg3.log 2>&1
+# LM-head fusion: launch list of the fused call and a full capture of lmh_gemm
+ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
+    -k "regex:lmh_gemm|qrita_tail" -c 6 --csv --log-file gpurun_out/prof/launches_lmhead.csv \
+    python tools/lmh_prof.py > /dev/null 2>&1
+ncu --set full --clock-control none --import-source on -k regex:lmh_gemm -s 1 -c 1 \
+    -o gpurun_out/prof/lmhead_gemm python tools/lmh_prof.py > gpurun_out/prof/lmhead_gemm.log 2>&1

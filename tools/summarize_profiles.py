@@ -38,7 +38,7 @@ def launches(cfg):
 
 
 summary = {}
-for cfg in ("cfg2", "cfg4", "cfg3", "cfg1", "cfg5", "cfg2copy"):
+for cfg in ("cfg2", "cfg4", "cfg3", "cfg1", "cfg5", "cfg2copy", "lmhead"):
     try:
         summary[cfg] = launches(cfg)
     except (OSError, StopIteration, KeyError) as e:
@@ -56,11 +56,15 @@ WANT = ["Kernel Name", "gpu__time_duration.sum", "dram__bytes_read.sum", "dram__
         "launch__shared_mem_per_block_dynamic", "launch__shared_mem_per_block_static",
         "launch__occupancy_limit_registers", "launch__occupancy_limit_shared_mem",
         "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum", "lts__t_sectors_srcunit_tex_op_read.sum",
-        "smsp__cycles_active.avg"]
+        "smsp__cycles_active.avg",
+        "TPC.TriageCompute.sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed",
+        "sm__mem_tensor_cycles_active.avg.pct_of_peak_sustained_active",
+        "l1tex__data_pipe_tc_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed"]
 SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
 traffic = {}
 for name, cfg, kern, how in (("fused_cfg2", "cfg2", "qrita_fused<float,3>", "-k regex:qrita_fused ... bench.py"),
-                             ("topp16_cfg3", "cfg3", "qrita_topp16", "-k regex:qrita_topp16 ... bench.py --config cfg3")):
+                             ("topp16_cfg3", "cfg3", "qrita_topp16", "-k regex:qrita_topp16 ... bench.py --config cfg3"),
+                             ("lmhead_gemm", "lmhead", "lmh_gemm<256,4>", "-k regex:lmh_gemm ... tools/lmh_prof.py")):
     rep = os.path.join(SRC, f"{name}.ncu-rep")
     if not os.path.exists(rep):
         continue
@@ -72,8 +76,12 @@ for name, cfg, kern, how in (("fused_cfg2", "cfg2", "qrita_fused<float,3>", "-k 
               float(v[i]) for i, k in enumerate(h) if k.startswith("smsp__average_warps_issue_stalled_") and
               k.endswith("_per_issue_active.ratio")}
     with open(os.path.join(DST, f"{tag}_ncu_full_{name}.json"), "w") as fh:
-        json.dump({"how": f"ncu --set full --clock-control none --import-source on {how} --steps 1 --warmup 3 "
-                          "--no-extras (-s 3 -c 1: one launch, cold caches)", "metrics": full,
+        hw = (f"ncu --set full --clock-control none --import-source on -k regex:lmh_gemm -s 1 -c 1 python "
+              "tools/lmh_prof.py (one launch of the fused call's GEMM, B=256 V=128256 d=4096, cold caches)"
+              if name == "lmhead_gemm" else
+              f"ncu --set full --clock-control none --import-source on {how} --steps 1 --warmup 3 "
+              "--no-extras (-s 3 -c 1: one launch, cold caches)")
+        json.dump({"how": hw, "metrics": full,
                    "top_stalls_per_issue": dict(sorted(stalls.items(), key=lambda t: -t[1])[:8])}, fh, indent=1)
     rd = float(full["dram__bytes_read.sum"][0]) * SCALE[full["dram__bytes_read.sum"][1]]
     wr = float(full["dram__bytes_write.sum"][0]) * SCALE[full["dram__bytes_write.sum"][1]]
