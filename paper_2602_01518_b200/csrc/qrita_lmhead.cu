@@ -124,7 +124,8 @@ __device__ __forceinline__ uint32_t lmh_key(uint32_t b) {
   return b ^ ((uint32_t)((int32_t)b >> 31) | 0x80000000u);
 }
 
-constexpr int kEpiWarps = 8;                    // two per TMEM lane quarter, each half of the columns
+constexpr int kEpiWarps = 8;
+constexpr int kMaxPlanRows = 4;                 // rows per CTA whose plan_begin runs up front                    // two per TMEM lane quarter, each half of the columns
 constexpr int kGemmThreads = 64 + 32 * kEpiWarps;
 
 __device__ __forceinline__ void epi_sync() {    // the epilogue warps only
@@ -152,7 +153,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) lmh_gemm(const __grid_constan
   __shared__ uint32_t s_mx[4][BN], s_cnt[4][BN];
   __shared__ __align__(16) float s_thr[BN];
   __shared__ PlanScratch s_sc;
-  __shared__ RowPlan s_pl;
+  __shared__ RowPlan s_pls[kMaxPlanRows];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int nk = a.d / kBK;
   const int vt = (a.vlimit + kBM - 1) / kBM, bt = (a.B + BN - 1) / BN;
@@ -257,23 +258,44 @@ __global__ void __launch_bounds__(kGemmThreads, 1) lmh_gemm(const __grid_constan
           if (et == 0) atomicAdd(&a.done[y], 1u);
         }
         if (i == 0) {
-          // every CTA plans rows blockIdx.x, blockIdx.x + gridDim.x, ... (qrita_prep's work) once the
-          // nst sample tiles are written (single batch tile: every CTA's first tile is in it)
+          // every CTA plans rows blockIdx.x, blockIdx.x + gridDim.x, ... (qrita_prep's work): the
+          // sample-independent part for all of them at once (one thread per row), the sample part
+          // once the nst sample tiles are written (one batch tile: every CTA's first tile is in it)
+          const int myrows = (a.B - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
+          for (int r = et; r < myrows && r < kMaxPlanRows; r += 32 * kEpiWarps)
+            plan_begin(P, (int)blockIdx.x + r * (int)gridDim.x, &s_pls[r]);
           if (et == 0)
             while (ld_acquire_gpu(&a.done[0]) < (uint32_t)a.nst) __nanosleep(64);
           epi_sync();
           uint32_t np = 0u;
           for (int row = blockIdx.x; row < a.B; row += gridDim.x, ++np) {
+            RowPlan &pl = s_pls[np < (uint32_t)kMaxPlanRows ? np : 0];
             const float *lr = a.logits + (size_t)row * a.ld;
-            float warm = 0.0f;  // independent loads pull the sample row into L1 first
-            for (int ii = et; ii < P.tree.n; ii += 32 * kEpiWarps) warm += __ldca(lr + ii);
-            if (warm == 1.2345e-38f) s_thr[0] = warm;  // keeps the loads
-            if (et == 0) plan_begin(P, row, &s_pl);
+            // the default sample (4096 = 32 leaves of 128): thread (leaf L, accumulator j) loads its
+            // 16 values at once and runs numpy's leaf loop in registers (plan_sample's order exactly)
+            const bool perfect = P.tree.n == 4096 && P.tree.n_leaves == 32;
+            if (perfect) {
+              const int L = et >> 3, j = et & 7;
+              float xv[16];
+#pragma unroll
+              for (int m = 0; m < 16; ++m) xv[m] = __ldcg(lr + 128 * L + j + 8 * m);
+              double r0 = (double)xv[0];
+              double r1 = __dmul_rn(r0, r0);
+#pragma unroll
+              for (int m = 1; m < 16; ++m) {
+                const double x = (double)xv[m];
+                r0 = __dadd_rn(r0, x);
+                r1 = __dadd_rn(r1, __dmul_rn(x, x));
+              }
+              s_sc.acc[0][L][j] = r0;
+              s_sc.acc[1][L][j] = r1;
+            }
+            if (np >= (uint32_t)kMaxPlanRows && et == 0) plan_begin(P, row, &pl);
             epi_sync();
-            plan_sample<float>(P, [&](int ii) -> float { return __ldca(lr + ii); }, lr, s_sc, &s_pl, 64);
+            plan_sample<float>(P, [&](int ii) -> float { return __ldcg(lr + ii); }, lr, s_sc, &pl, 64, perfect);
             epi_sync();
             if (et == 0) {
-              P.plans[row] = s_pl;
+              P.plans[row] = pl;
               uint4 *ag = reinterpret_cast<uint4 *>(P.agg + row);
               ag[0] = make_uint4(0u, 0u, 0u, 0xffffffffu);  // count, maxkey, minkey 0 (fused kernel's), nf_col
               ag[1] = make_uint4(0u, 0u, 0u, 0u);

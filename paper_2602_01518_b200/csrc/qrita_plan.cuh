@@ -176,20 +176,23 @@ __device__ __forceinline__ void plan_begin(const Params &P, int row, RowPlan *ou
 
 template <typename T, class SampleAt>
 __device__ void plan_sample(const Params &P, SampleAt xs, const T *a, PlanScratch &sc, RowPlan *out,
-                            int tid_base = 0) {
-  const int tid = (int)threadIdx.x - tid_base;  // the kThreads-thread group runs from warp tid_base / 32
+                            int tid_base = 0, bool leaves_done = false) {
+  // tid_base: the kThreads-thread group runs from warp tid_base / 32; leaves_done: the caller already
+  // filled sc.acc with the leaf loop below (the default 4096-sample perfect tree only)
+  const int tid = (int)threadIdx.x - tid_base;
   if (!out->has_thr) return;  // uniform per group (written before the caller's barrier)
   const PwTree &tr = P.tree;
   const int n = tr.n;
   const int nl = tr.n_leaves;
   if (nl > 0) {
     // numpy's 8-accumulator leaf loop, one thread per (leaf, accumulator)
-    for (int q = tid; q < nl * 8; q += kThreads) {
+    for (int q = leaves_done ? nl * 8 : tid; q < nl * 8; q += kThreads) {
       const int L = q >> 3, j = q & 7;
       const int o = tr.leaf_off[L], m = tr.leaf_len[L];
       if (m >= 8) {
         double r0 = (double)xs(o + j);
         double r1 = __dmul_rn(r0, r0);
+#pragma unroll 8  // independent loads in flight (global / L2-resident samples), same summation order
         for (int i = 8; i < m - (m % 8); i += 8) {
           const double x = (double)xs(o + i + j);
           r0 = __dadd_rn(r0, x);
