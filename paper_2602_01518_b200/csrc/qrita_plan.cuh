@@ -192,7 +192,6 @@ __device__ void plan_sample(const Params &P, SampleAt xs, const T *a, PlanScratc
       if (m >= 8) {
         double r0 = (double)xs(o + j);
         double r1 = __dmul_rn(r0, r0);
-#pragma unroll 8  // independent loads in flight (global / L2-resident samples), same summation order
         for (int i = 8; i < m - (m % 8); i += 8) {
           const double x = (double)xs(o + i + j);
           r0 = __dadd_rn(r0, x);
