@@ -532,10 +532,8 @@ __global__ void __launch_bounds__(kT) tp_write(const T *logits, int64_t ld_in, T
   if (tid == 0 && kept_count) kept_count[r] = (int32_t)nkept;
 }
 
-// The exact answer on one candidate row (<= kSmallW entries): sort by (value desc, global column
-// asc) in shared memory, top-k prefix, then — p < 1 — the survivors' exact fixed-point normaliser
-// and prefix masses (oracle.py:70-89): the first prefix whose exactly rounded sum reaches p, all of
-// them when fsum(survivors) <= p.  Writes the kept global columns (kidx_c) and their count (kc_c).
+// Candidate rows up to kSmallW entries (world * kmax) are resolved in shared memory from sorted
+// per-rank lists (tp_pack_sorted + tp_merge_resolve); wider ones by the single-GPU kernels.
 constexpr int kSmallW = 16384;
 
 // Descending bitonic sort of NT * EPT composites: blocked in registers (element t * EPT + j in
@@ -595,14 +593,55 @@ __device__ __forceinline__ void bitonic_desc(unsigned long long *sk) {
   __syncthreads();
 }
 
-// NT threads sort NT * EPT >= W entries; the mass scan runs on the first kThreads of them.
-template <int NT, int EPT>
-__global__ void __launch_bounds__(NT) tp_small_resolve(const uint32_t *recv, size_t send_words, int B4, int B,
-                                                          int kmax, int world, const int64_t *kk,
-                                                          const double *pp, TpRow *rows, int32_t *kidx_c,
-                                                          int32_t *kc_c, int W) {
+// The rank's candidates of row blockIdx.x sorted by (value desc, global column asc): 64-bit
+// (order key, ~global column) composites, bitonic in registers / shuffles / shared memory (NT * EPT
+// slots >= kmax), so the gathered lists only need merging.  send = [counts | keys | columns].
+template <typename T, int NT, int EPT>
+__global__ void __launch_bounds__(NT) tp_pack_sorted(const T *logits, int64_t ld, int64_t offset, int kmax,
+                                                    const int32_t *kc, const int32_t *kidx, uint32_t *send, int B4,
+                                                    int B) {
   extern __shared__ unsigned long long sk[];  // [NT * EPT]
-  constexpr int Wp = NT * EPT;
+  constexpr int Kp = NT * EPT;
+  const int r = blockIdx.x, tid = threadIdx.x;
+  const int cnt = kc[r];
+  const T *row = logits + (size_t)r * ld;
+  for (int i = tid; i < Kp; i += NT) {
+    unsigned long long c = 0ull;  // pads sort after every real entry
+    if (i < cnt) {
+      const int col = kidx[(size_t)r * kmax + i];
+      c = ((unsigned long long)key_at(row, col) << 32) | (0xffffffffu - (uint32_t)(offset + col));
+    }
+    sk[i] = c;
+  }
+  __syncthreads();
+  bitonic_desc<NT, EPT>(sk);
+  uint32_t *keys = send + B4 + (size_t)r * kmax;
+  uint32_t *gid = send + B4 + (size_t)B * kmax + (size_t)r * kmax;
+  for (int i = tid; i < kmax; i += NT) {
+    const unsigned long long c = i < cnt ? sk[i] : 0ull;
+    keys[i] = i < cnt ? (uint32_t)(c >> 32) : 0u;
+    gid[i] = i < cnt ? 0xffffffffu - (uint32_t)c : 0xffffffffu;
+  }
+  if (tid == 0) send[r] = (uint32_t)cnt;
+}
+
+constexpr int kMergeT = 512;
+
+// The exact answer on one candidate row from the ranks' sorted lists: the global rank of a list's
+// i-th entry is i plus, per other list, the count of its entries above it (binary search); the
+// entries ranked below k land in rank order (the global top-k, sorted), then — p < 1 — the
+// survivors' exact fixed-point normaliser and prefix masses (oracle.py:70-89): the first prefix
+// whose exactly rounded sum reaches p, all of them when fsum(survivors) <= p.  Writes the kept
+// global columns (kidx_c) and their count (kc_c).
+__global__ void __launch_bounds__(kMergeT) tp_merge_resolve(const uint32_t *recv, size_t send_words, int B4, int B,
+                                                           int kmax, int world, int scap, int lp, int wp,
+                                                           const int64_t *kk, const double *pp, TpRow *rows,
+                                                           int32_t *kidx_c, int32_t *kc_c, int W) {
+  // lp: list slots (power of two >= kmax); wp: lists (power of two >= world); lp == 0: no merge tree
+  extern __shared__ unsigned long long sk[];  // rank path: [W] lists | [scap] sorted | offsets
+  unsigned long long *srt = world > 1 ? sk + W : sk;
+  uint32_t *off = reinterpret_cast<uint32_t *>(sk + W + (world > 1 ? scap : 0));  // [world + 1]
+  __shared__ uint32_t s_off[kMaxWorld + 1];
   __shared__ Fx scan_buf[kWarps];
   __shared__ uint32_t s_L, s_keep;
   const int r = blockIdx.x, tid = threadIdx.x;
@@ -619,36 +658,105 @@ __global__ void __launch_bounds__(NT) tp_small_resolve(const uint32_t *recv, siz
     }
     return;
   }
-  // the ranks' candidate lists straight from the all-gather buffer, as (key, ~global column)
-  // composites; pads (0) sort after every real entry
-  for (int i = tid; i < Wp; i += NT) sk[i] = 0ull;
-  __syncthreads();
-  uint32_t n = 0u;
-  for (int g = 0; g < world; ++g) {
-    const uint32_t *sg = recv + (size_t)g * send_words;
-    const uint32_t ng = sg[r];
-    const uint32_t *keys = sg + B4 + (size_t)r * kmax;
-    const uint32_t *gid = sg + B4 + (size_t)B * kmax + (size_t)r * kmax;
-    for (uint32_t i = tid; i < ng; i += NT) sk[n + i] = ((unsigned long long)keys[i] << 32) | (0xffffffffu - gid[i]);
-    n += ng;
+  if (tid == 0) {
+    uint32_t acc = 0u;
+    for (int g = 0; g < world; ++g) {
+      s_off[g] = acc;
+      acc += recv[(size_t)g * send_words + r];
+    }
+    s_off[world] = acc;
   }
   __syncthreads();
-  bitonic_desc<NT, EPT>(sk);
+  const uint32_t n = s_off[world];
   const int k = (int)min((int64_t)n, kk[r]);
+  if (world > 1 && lp > 0 && k <= lp) {
+    // merge tree: list g in slots [g * lp, (g + 1) * lp), padded with 0 (below every entry); each
+    // level merges list pairs into the top lp of the two (half-cleaner against the reversed partner,
+    // then a bitonic merge) until list 0 holds the global top lp in order
+    const int lg = 31 - __clz(lp);  // lp = 1 << lg
+    for (int e = tid; e < wp * lp; e += kMergeT) {
+      const int g = e >> lg, i = e & (lp - 1);
+      unsigned long long c = 0ull;
+      if (g < world && (uint32_t)i < s_off[g + 1] - s_off[g]) {
+        const uint32_t *sg = recv + (size_t)g * send_words;
+        c = ((unsigned long long)sg[B4 + (size_t)r * kmax + i] << 32) |
+            (0xffffffffu - sg[B4 + (size_t)B * kmax + (size_t)r * kmax + i]);
+      }
+      sk[e] = c;
+    }
+    __syncthreads();
+    for (int half = 1; half < wp; half <<= 1) {
+      const int pairs = wp / (2 * half);
+      for (int e = tid; e < pairs * lp; e += kMergeT) {
+        const int j = e >> lg, i = e & (lp - 1);
+        unsigned long long *A = sk + (size_t)(2 * j * half) * lp, *Bl = sk + (size_t)(2 * j * half + half) * lp;
+        const unsigned long long a = A[i], b = Bl[lp - 1 - i];
+        A[i] = a > b ? a : b;
+      }
+      __syncthreads();
+      for (int stride = lp >> 1; stride > 0; stride >>= 1) {
+        for (int e = tid; e < pairs * (lp >> 1); e += kMergeT) {
+          const int j = e >> (lg - 1), t = e & ((lp >> 1) - 1);
+          unsigned long long *A = sk + (size_t)(2 * j * half) * lp;
+          const int i = ((t & ~(stride - 1)) << 1) | (t & (stride - 1));
+          const unsigned long long x = A[i], y = A[i + stride];
+          if (x < y) { A[i] = y; A[i + stride] = x; }
+        }
+        __syncthreads();
+      }
+    }
+    srt = sk;  // list 0: the global top lp >= k, descending
+  } else {
+  if (tid == 0)
+    for (int g = 0; g <= world; ++g) off[g] = s_off[g];
+  __syncthreads();
+  for (int g = 0; g < world; ++g) {
+    const uint32_t *sg = recv + (size_t)g * send_words;
+    const uint32_t o = off[g], ng = off[g + 1] - o;
+    const uint32_t *keys = sg + B4 + (size_t)r * kmax;
+    const uint32_t *gid = sg + B4 + (size_t)B * kmax + (size_t)r * kmax;
+    for (uint32_t i = tid; i < ng; i += kMergeT) sk[o + i] = ((unsigned long long)keys[i] << 32) | (0xffffffffu - gid[i]);
+  }
+  __syncthreads();
+  if (world > 1) {
+    for (uint32_t e = tid; e < n; e += kMergeT) {
+      int lo = 0, hi = world;  // list of e: off[g] <= e < off[g + 1]
+      while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (off[mid] <= e) lo = mid; else hi = mid;
+      }
+      const int g = lo;
+      uint32_t rank = e - off[g];
+      if (rank >= (uint32_t)k) continue;
+      const unsigned long long c = sk[e];
+      for (int h = 0; h < world && rank < (uint32_t)k; ++h) {
+        if (h == g) continue;
+        uint32_t a = off[h], z = off[h + 1];  // entries of list h above c: a prefix (descending)
+        while (a < z) {
+          const uint32_t mid = (a + z) >> 1;
+          if (sk[mid] > c) a = mid + 1; else z = mid;
+        }
+        rank += a - off[h];
+      }
+      if (rank < (uint32_t)k) srt[rank] = c;
+    }
+    __syncthreads();
+  }
+  }
   const double p = pp[r];
   if (tid == 0) s_keep = (uint32_t)k;
   if (p < 1.0 && tid < kThreads) {
-    const double m = value_of_key((uint32_t)(sk[0] >> 32));
+    const double m = value_of_key((uint32_t)(srt[0] >> 32));
     const int E = (k + kThreads - 1) / kThreads, q0 = tid * E;
     Fx d = fx_zero();
     for (int j = 0; j < E; ++j)
-      if (q0 + j < k) d = fx_add(d, fx_from_double(exp(value_of_key((uint32_t)(sk[q0 + j] >> 32)) - m)));
+      if (q0 + j < k) d = fx_add(d, fx_from_double(exp(value_of_key((uint32_t)(srt[q0 + j] >> 32)) - m)));
     Fx D_fx;
     (void)block_exscan_fx(d, scan_buf, D_fx);
     const double D = fx_to_double(D_fx);
     Fx ms = fx_zero();
     for (int j = 0; j < E; ++j)
-      if (q0 + j < k) ms = fx_add(ms, fx_from_double(exp(value_of_key((uint32_t)(sk[q0 + j] >> 32)) - m) / D));
+      if (q0 + j < k) ms = fx_add(ms, fx_from_double(exp(value_of_key((uint32_t)(srt[q0 + j] >> 32)) - m) / D));
     tsync();  // scan_buf reuse
     Fx total;
     Fx pre = block_exscan_fx(ms, scan_buf, total);
@@ -657,7 +765,7 @@ __global__ void __launch_bounds__(NT) tp_small_resolve(const uint32_t *recv, siz
     const Fx Tp = fx_round_threshold(p);
     for (int j = 0; j < E; ++j) {
       if (q0 + j < k) {
-        pre = fx_add(pre, fx_from_double(exp(value_of_key((uint32_t)(sk[q0 + j] >> 32)) - m) / D));
+        pre = fx_add(pre, fx_from_double(exp(value_of_key((uint32_t)(srt[q0 + j] >> 32)) - m) / D));
         if (fx_ge(pre, Tp)) { atomicMin(&s_L, (uint32_t)(q0 + j + 1)); break; }
       }
     }
@@ -666,7 +774,7 @@ __global__ void __launch_bounds__(NT) tp_small_resolve(const uint32_t *recv, siz
   }
   __syncthreads();
   const int L = (int)s_keep;
-  for (int i = tid; i < L; i += NT) kidx_c[(size_t)r * W + i] = (int32_t)(0xffffffffu - (uint32_t)sk[i]);
+  for (int i = tid; i < L; i += kMergeT) kidx_c[(size_t)r * W + i] = (int32_t)(0xffffffffu - (uint32_t)srt[i]);
   if (tid == 0) kc_c[r] = L;
 }
 
@@ -768,19 +876,49 @@ cudaError_t smem_optin(K kernel, int *slots) {
   int v = 0;
   return per_device_once(slots, [&](int, int &out) {
     out = 1;
-    return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(128u << 10));
+    return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(210u << 10));
   }, v);
 }
 
-template <int NT, int EPT>
-cudaError_t launch_small(const uint32_t *recv, const TpLayout &L, int B, int world, const int64_t *k, const double *p,
-                         TpRow *rows, int32_t *kidx_c, int32_t *kc_c, cudaStream_t st) {
+template <typename T, int NT, int EPT>
+cudaError_t launch_pack(const T *x, int64_t ld, int64_t offset, const TpLayout &L, const int32_t *kc,
+                        const int32_t *kidx, uint32_t *send, int B, cudaStream_t st) {
   constexpr size_t sbytes = (size_t)NT * EPT * 8;
   static int optin[kMaxDevices] = {};
-  if (sbytes > (48u << 10) && smem_optin(tp_small_resolve<NT, EPT>, optin) != cudaSuccess) return cudaErrorUnknown;
-  tp_small_resolve<NT, EPT><<<B, NT, sbytes, st>>>(recv, L.send_words, L.B4, B, L.kmax, world, k, p, rows, kidx_c,
-                                                   kc_c, L.W);
+  if (sbytes > (48u << 10) && smem_optin(tp_pack_sorted<T, NT, EPT>, optin) != cudaSuccess) return cudaErrorUnknown;
+  tp_pack_sorted<T, NT, EPT><<<B, NT, sbytes, st>>>(x, ld, offset, L.kmax, kc, kidx, send, L.B4, B);
   return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t launch_pack_sorted(const T *x, int64_t ld, int64_t offset, const TpLayout &L, const int32_t *kc,
+                               const int32_t *kidx, uint32_t *send, int B, cudaStream_t st) {
+  const int km = L.kmax;
+  if (km <= 256) return launch_pack<T, 256, 1>(x, ld, offset, L, kc, kidx, send, B, st);
+  if (km <= 512) return launch_pack<T, 256, 2>(x, ld, offset, L, kc, kidx, send, B, st);
+  if (km <= 1024) return launch_pack<T, 256, 4>(x, ld, offset, L, kc, kidx, send, B, st);
+  if (km <= 2048) return launch_pack<T, 256, 8>(x, ld, offset, L, kc, kidx, send, B, st);
+  if (km <= 4096) return launch_pack<T, 256, 16>(x, ld, offset, L, kc, kidx, send, B, st);
+  if (km <= 8192) return launch_pack<T, 512, 16>(x, ld, offset, L, kc, kidx, send, B, st);
+  return launch_pack<T, 1024, 16>(x, ld, offset, L, kc, kidx, send, B, st);
+}
+
+// tp_merge_resolve's merge tree: list slots (power of two >= kmax) and lists (power of two >= world)
+inline void merge_tree_shape(const TpLayout &L, int world, int &lp, int &wp) {
+  lp = 1;
+  while (lp < L.kmax) lp <<= 1;
+  wp = 1;
+  while (wp < world) wp <<= 1;
+  if (world < 2 || (size_t)lp * wp * 8 > (200u << 10)) lp = 0;  // rank path only
+}
+
+// shared memory of tp_merge_resolve: the rank path's lists + sorted top-k + offsets, or the tree
+inline size_t merge_smem(const TpLayout &L, int world, int scap) {
+  int lp, wp;
+  merge_tree_shape(L, world, lp, wp);
+  const size_t rank_path = (size_t)L.W * 8 + (world > 1 ? (size_t)scap * 8 : 0) + (size_t)(world + 1) * 4;
+  const size_t tree = (size_t)lp * wp * 8;
+  return rank_path > tree ? rank_path : tree;
 }
 
 template <typename T>
@@ -800,7 +938,9 @@ int run_tp(const void *logits, int64_t ld_in, int dtype, int B, int Vr, int Vg, 
       return QRITA_ECUDA;
   }
   const T *x = (const T *)logits;
-  const bool small = L.W <= kSmallW;  // candidate rows resolved by tp_small_resolve
+  const int scap = L.W < ((k_cap + 3) & ~3) ? L.W : ((k_cap + 3) & ~3);  // sorted top-k slots
+  // candidate rows resolved in shared memory (tp_pack_sorted + tp_merge_resolve)
+  const bool small = L.W <= kSmallW && merge_smem(L, world, scap) <= (210u << 10);
   int64_t *k_loc = (int64_t *)at(L.k_loc), *k_c = (int64_t *)at(L.k_c);
   double *p_one = (double *)at(L.p_one), *p_c = (double *)at(L.p_c);
   TpRow *rows = (TpRow *)at(L.rows);
@@ -817,28 +957,29 @@ int run_tp(const void *logits, int64_t ld_in, int dtype, int B, int Vr, int Vg, 
                           (int32_t *)at(L.kc_s), nullptr, at(L.ws0), L.ws0_bytes, 0, 4096, (qrita_stream_t)st,
                           nullptr, nullptr, nullptr, nullptr, (int32_t *)at(L.kidx_s), L.kmax);
   if (rc != QRITA_OK) return rc;
-  tp_pack<T><<<B, kT, small ? 0 : bm_bytes, st>>>(x, ld_in, Vr, offset, L.kmax, (const int32_t *)at(L.kc_s),
-                                      (const int32_t *)at(L.kidx_s), (uint32_t *)at(L.send), L.B4, B, small ? 0 : 1);
-  if (cudaGetLastError() != cudaSuccess) return QRITA_ECUDA;
+  if (small) {
+    if (launch_pack_sorted<T>(x, ld_in, offset, L, (const int32_t *)at(L.kc_s), (const int32_t *)at(L.kidx_s),
+                              (uint32_t *)at(L.send), B, st) != cudaSuccess)
+      return QRITA_ECUDA;
+  } else {
+    tp_pack<T><<<B, kT, bm_bytes, st>>>(x, ld_in, Vr, offset, L.kmax, (const int32_t *)at(L.kc_s),
+                                        (const int32_t *)at(L.kidx_s), (uint32_t *)at(L.send), L.B4, B, 1);
+    if (cudaGetLastError() != cudaSuccess) return QRITA_ECUDA;
+  }
   if (comm->all_gather(at(L.send), at(L.recv), 4 * L.send_words, (qrita_stream_t)st, comm->ctx) != 0)
     return QRITA_ENCCL;
   // (2) the exact answer on the gathered candidates (same on every rank): a shared-memory sort for
   //     candidate rows up to kSmallW entries, else the single-GPU kernels
   if (small) {
-    const uint32_t *recv = (const uint32_t *)at(L.recv);
-    int32_t *kidx_c = (int32_t *)at(L.kidx_c), *kc_c = (int32_t *)at(L.kc_c);
-    cudaError_t e;
-    if (L.W <= 1024)
-      e = launch_small<256, 4>(recv, L, B, world, k, p, rows, kidx_c, kc_c, st);
-    else if (L.W <= 2048)
-      e = launch_small<256, 8>(recv, L, B, world, k, p, rows, kidx_c, kc_c, st);
-    else if (L.W <= 4096)
-      e = launch_small<256, 16>(recv, L, B, world, k, p, rows, kidx_c, kc_c, st);
-    else if (L.W <= 8192)
-      e = launch_small<512, 16>(recv, L, B, world, k, p, rows, kidx_c, kc_c, st);
-    else
-      e = launch_small<1024, 16>(recv, L, B, world, k, p, rows, kidx_c, kc_c, st);
-    if (e != cudaSuccess) return QRITA_ECUDA;
+    const size_t sb = merge_smem(L, world, scap);
+    static int optin_merge[kMaxDevices] = {};
+    if (sb > (48u << 10) && smem_optin(tp_merge_resolve, optin_merge) != cudaSuccess) return QRITA_ECUDA;
+    int lp, wp;
+    merge_tree_shape(L, world, lp, wp);
+    tp_merge_resolve<<<B, kMergeT, sb, st>>>((const uint32_t *)at(L.recv), L.send_words, L.B4, B, L.kmax, world,
+                                             scap, lp, wp, k, p, rows, (int32_t *)at(L.kidx_c), (int32_t *)at(L.kc_c),
+                                             L.W);
+    if (cudaGetLastError() != cudaSuccess) return QRITA_ECUDA;
   } else {
     tp_merge<<<B, kT, 0, st>>>((const uint32_t *)at(L.recv), L.send_words, L.B4, B, L.kmax, world, L.W, k, p, rows,
                                (float *)at(L.cval), (uint32_t *)at(L.cgid), k_c, p_c);
