@@ -561,7 +561,7 @@ def bench_tp(args, rank: int, world: int, dev):
                      "alg_bytes_per_launch": alg},
         "exchange_bytes_per_row_per_rank": 8 * kmax + 4,
         "clocks": clk.summary(),
-        "gpu_launches": 5 * args.steps,  # prep, local fused, pack, small resolve, write (+ NCCL all-gather)
+        "gpu_launches": 5 * args.steps,  # prep, local fused, sorted pack, merge resolve, write (+ NCCL all-gather)
     }
     comm.close()
     if world > 1:
