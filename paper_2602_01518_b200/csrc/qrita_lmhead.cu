@@ -592,15 +592,22 @@ int qrita_lmhead_topk_topp(const void *hidden, int64_t ld_h, const void *weight,
   const int bn = batch_tile(B), bt = (B + bn - 1) / bn, nst = (ns + kBM - 1) / kBM;
   const int vt = (V + kBM - 1) / kBM;
   const int grid = vt * bt < sm_count() ? vt * bt : sm_count();
-  if (bt == 1 && nst <= grid && !(getenv("QRITA_LMH_PREP"))) {
+  bool one_launch = bt == 1 && nst <= grid && !(getenv("QRITA_LMH_PREP"));
+  if (one_launch) {
     // one launch: the sample tiles come first, their CTAs plan the rows, every epilogue waits for
     // its batch tile's plans (the MMAs of the next tile run meanwhile)
     uint32_t *cnt = (uint32_t *)(ws + LL.counters);
     if (cudaMemsetAsync(cnt, 0, 2 * 4 * (size_t)bt, st) != cudaSuccess) return QRITA_ECUDA;
-    a.plan_rows = 1; a.nst = nst; a.done = cnt; a.ready = cnt + bt;
-    rc = run_gemm(hidden, ld_h, weight, ld_w, a, P, st);
-    if (rc != QRITA_OK) return rc;
-  } else {
+    Args a1 = a;
+    a1.plan_rows = 1; a1.nst = nst; a1.done = cnt; a1.ready = cnt + bt;
+    if (run_gemm(hidden, ld_h, weight, ld_w, a1, P, st) != QRITA_OK) {
+      // the cooperative launch needs every CTA resident at once (an MPS share of the SMs may not
+      // allow it): take the three-launch path instead
+      (void)cudaGetLastError();
+      one_launch = false;
+    }
+  }
+  if (!one_launch) {
     // (1) the sample prefix of every row: the same GEMM tiles as the full pass (bit-identical values)
     Args as = a;
     as.plans = nullptr; as.vlimit = ns; as.logits = sample; as.ld = kSample;
