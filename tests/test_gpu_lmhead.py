@@ -37,7 +37,8 @@ def _kept_sets(idx, cnt):
     return [np.sort(idx[r, :cnt[r]]) for r in range(len(cnt))]
 
 
-@pytest.mark.parametrize("b,v,d", [(4, 4096, 128), (37, 32000, 256), (130, 9000, 128), (300, 5000, 64)])
+@pytest.mark.parametrize("b,v,d", [(4, 4096, 128), (37, 32000, 256), (130, 9000, 128), (300, 5000, 64),
+                                   (9, 1000, 64), (20, 2500, 128)])
 def test_fused_kept_sets_exact(cuda_device, b, v, d):
     h, w = _operands(b, v, d, 7 * b + v)
     if b > 5:
@@ -77,3 +78,21 @@ def test_fused_invalid_rows_raise(cuda_device):
         lm_head_topk_topp(h, w, torch.tensor([5, 0, 5, 5]), 0.9, check=True)
     with pytest.raises(ValueError):
         lm_head_logits(h[:, :60].contiguous(), w[:, :60].contiguous())
+
+
+def test_fused_metrics_match_the_truncation_path(cuda_device):
+    """The fused epilogue plans from the same (bit-identical) sample logits and counts outliers with
+    the same predicate as the streaming pass, so the reference's per-row metrics agree."""
+    b, v, d = 24, 20000, 128
+    h, w = _operands(b, v, d, 99)
+    rng = np.random.default_rng(4)
+    k = torch.from_numpy(rng.integers(1, 600, b).astype(np.int64))
+    p = torch.from_numpy(rng.uniform(0.4, 0.99, b))
+    mf = Q.ops.metrics_buffer(b, "cuda")
+    logits, kidx, kc = lm_head_topk_topp(h, w, k, p, metrics=mf)
+    mr = Q.ops.metrics_buffer(b, "cuda")
+    Q.topk_topp_indices(logits, k.cuda(), p.cuda(), metrics=mr)
+    got, want = Q.ops.decode_metrics(mf), Q.ops.decode_metrics(mr)
+    for r in range(b):
+        for key in ("trunc_hit", "outlier_count", "fallback_used", "kept_count"):
+            assert got[r][key] == want[r][key], (r, key, got[r][key], want[r][key])
