@@ -175,6 +175,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) lmh_gemm(const __grid_constan
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = tmem_base;
+  pdl_launch_dependents();  // the row tails may be scheduled (they wait for this grid's results)
 
   if (warp == 0) {
     if (lane == 0) {  // TMA producer
@@ -639,9 +640,21 @@ int qrita_lmhead_topk_topp(const void *hidden, int64_t ld_h, const void *weight,
     return cudaFuncSetAttribute(qrita_tail<float, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTailDynSmem);
   }, dummy);
   if (e != cudaSuccess) return QRITA_ECUDA;
-  if (flags & QRITA_SEARCH_BINARY) qrita_tail<float, 1><<<B, kThreads, kTailDynSmem, st>>>(P);
-  else qrita_tail<float, 3><<<B, kThreads, kTailDynSmem, st>>>(P);
-  return cudaGetLastError() == cudaSuccess ? QRITA_OK : QRITA_ECUDA;
+  // programmatic dependent launch: the tail CTAs take the SMs the GEMM's last round leaves idle and
+  // wait there (griddepcontrol.wait in qrita_tail) for the GEMM's results
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)B);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = kTailDynSmem;
+  cfg.stream = st;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  e = (flags & QRITA_SEARCH_BINARY) ? cudaLaunchKernelEx(&cfg, qrita_tail<float, 1>, (const Params)P)
+                                    : cudaLaunchKernelEx(&cfg, qrita_tail<float, 3>, (const Params)P);
+  return e == cudaSuccess ? QRITA_OK : QRITA_ECUDA;
 }
 
 }  // extern "C"
