@@ -614,7 +614,11 @@ __global__ void __launch_bounds__(NT) tp_pack_sorted(const T *logits, int64_t ld
     sk[i] = c;
   }
   __syncthreads();
-  bitonic_desc<NT, EPT>(sk);
+  // the shard call's bin-sort resolve usually emits its kept columns already in this order: sort
+  // only when some neighbour pair is out of order
+  int unsorted = 0;
+  for (int i = tid; i + 1 < cnt; i += NT) unsorted |= sk[i] < sk[i + 1] ? 1 : 0;
+  if (__syncthreads_or(unsorted)) bitonic_desc<NT, EPT>(sk);
   uint32_t *keys = send + B4 + (size_t)r * kmax;
   uint32_t *gid = send + B4 + (size_t)B * kmax + (size_t)r * kmax;
   for (int i = tid; i < kmax; i += NT) {
