@@ -277,7 +277,10 @@ def main():
     import torch
     import torch.distributed as dist
 
+    import ctypes
+
     import paper_2602_01518_b200 as Q
+    from paper_2602_01518_b200 import _native as N
     from paper_2602_01518_b200.sortsel import torch_sort_topk_topp
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -461,7 +464,11 @@ def main():
             if i >= 2:
                 tt.append(e0.elapsed_time(e1))
         h2d = x_host.numel() * x_host.element_size() + b * 16
-        d2h = o_host.numel() * o_host.element_size() + b * 8  # masked logits + status words
+        # what the host pipeline downloads: the masked rows, or (sparse form, every row top-k with
+        # k <= 4096) each row's kept columns + counts; plus the status words
+        d2h = int(N.load().qrita_host_download_bytes(b, v, 0 if dtype == "f32" else 1,
+                                                     ctypes.c_void_p(k_host.data_ptr()),
+                                                     ctypes.c_void_p(o_host.data_ptr()))) + b * 8
         e2e_ms = sharded_max(statistics.mean(tt), world, dev)
         line["e2e"] = {"value": total_rows / (e2e_ms / 1e3), "unit": "rows/s", "h2d_bytes_per_step": h2d,
                        "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms,

@@ -39,7 +39,7 @@ EXPORTED_SYMBOLS = (
     "qrita_get_status_host", "qrita_strerror", "qrita_version",
     "qrita_tp_workspace_bytes", "qrita_topk_topp_tp_comm", "qrita_topk_topp_tp", "qrita_nccl_unique_id",
     "qrita_nccl_comm_init", "qrita_nccl_comm_destroy", "qrita_copy_sync", "qrita_sigma_table",
-    "qrita_row_stats", "qrita_lmhead_logits", "qrita_lmhead_workspace_bytes", "qrita_lmhead_topk_topp",
+    "qrita_row_stats", "qrita_host_download_bytes", "qrita_lmhead_logits", "qrita_lmhead_workspace_bytes", "qrita_lmhead_topk_topp",
 )
 
 
@@ -120,6 +120,8 @@ def load() -> ctypes.CDLL:
     lib.qrita_sigma_table.restype = i32
     lib.qrita_row_stats.argtypes = [vp, i64, i32, i32, i32, i32, vp, vp]
     lib.qrita_row_stats.restype = i32
+    lib.qrita_host_download_bytes.argtypes = [i32, i32, i32, vp, vp]
+    lib.qrita_host_download_bytes.restype = i64
     lib.qrita_lmhead_logits.argtypes = [vp, i64, vp, i64, i32, i32, i32, vp, i64, vp]
     lib.qrita_lmhead_logits.restype = i32
     lib.qrita_lmhead_workspace_bytes.argtypes = [i32, i32]

@@ -9,6 +9,7 @@
 #include <atomic>
 #include <condition_variable>
 #include <mutex>
+#include <functional>
 #include <thread>
 #include <vector>
 
@@ -117,6 +118,8 @@ struct HostPipe {
   void *stage_in[2] = {nullptr, nullptr}, *stage_out[2] = {nullptr, nullptr};
   size_t stage_bytes = 0;
   cudaEvent_t in_free[2] = {nullptr, nullptr}, out_ready[2] = {nullptr, nullptr};
+  int32_t *kept_host = nullptr;  // sparse downloads: kept columns [B][kcap] | counts [B] (page-locked)
+  size_t kept_host_bytes = 0;
 };
 std::mutex g_host_mu;
 HostPipe g_host_pipe[64];
@@ -167,6 +170,27 @@ class CopyPool {
     static CopyPool *pool = new CopyPool();  // never destroyed: its threads end with the process
     return *pool;
   }
+  // fn(0 .. n-1) over the pool (items claimed one at a time; the caller is one of the workers)
+  void parallel_for(size_t n, const std::function<void(size_t)> &fn) {
+    if (n < 2 || nthreads_ == 0) {
+      for (size_t i = 0; i < n; ++i) fn(i);
+      return;
+    }
+    std::lock_guard<std::mutex> call(call_mu_);
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      fn_ = &fn;
+      items_ = n;
+      next_.store(0);
+      active_ = nthreads_;
+      ++gen_;
+    }
+    cv_work_.notify_all();
+    run_pieces();
+    std::unique_lock<std::mutex> lk(mu_);
+    cv_done_.wait(lk, [&] { return active_ == 0; });
+    fn_ = nullptr;
+  }
   void copy(void *d, const void *s, size_t n) {
     if (n < (1u << 20) || nthreads_ == 0) {
       memcpy(d, s, n);
@@ -175,6 +199,7 @@ class CopyPool {
     std::lock_guard<std::mutex> call(call_mu_);
     {
       std::lock_guard<std::mutex> lk(mu_);
+      fn_ = nullptr;
       dst_ = (uint8_t *)d;
       src_ = (const uint8_t *)s;
       bytes_ = n;
@@ -202,6 +227,10 @@ class CopyPool {
     for (int i = 0; i < n; ++i) std::thread([this] { worker(); }).detach();
   }
   void run_pieces() {
+    if (fn_) {
+      for (size_t i; (i = next_.fetch_add(1)) < items_;) (*fn_)(i);
+      return;
+    }
     for (;;) {
       const size_t off = next_.fetch_add(1) * piece_;
       if (off >= bytes_) return;
@@ -226,9 +255,30 @@ class CopyPool {
   uint64_t gen_ = 0;
   uint8_t *dst_ = nullptr;
   const uint8_t *src_ = nullptr;
-  size_t bytes_ = 0, piece_ = 0;
+  size_t bytes_ = 0, piece_ = 0, items_ = 0;
+  const std::function<void(size_t)> *fn_ = nullptr;
   std::atomic<size_t> next_{0};
 };
+
+// Sparse downloads (host pipeline): when every row keeps at most k < V entries (top-k active, k small),
+// the kernel writes each row's kept columns instead of the masked row; only those come back over
+// PCIe and the host builds the masked rows from its own copy of the logits (-inf fill + copy of the
+// kept entries, bit-identical).  Returns the kept-column slots per row (a multiple of 4), or 0 when
+// the batch is not eligible.
+constexpr int64_t kSparseCap = 4096;
+int sparse_slots(int B, int V, int dtype, const int64_t *k_host) {
+  if (getenv("QRITA_HOST_DENSE")) return 0;
+  int64_t kmax = 0;
+  for (int r = 0; r < B; ++r) {
+    const int64_t k = k_host[r];
+    if (!(k >= 1 && k < (int64_t)V)) return 0;  // top-p-only / pass-through / invalid rows: dense
+    kmax = k > kmax ? k : kmax;
+  }
+  const int64_t slots = (kmax + 3) & ~(int64_t)3;
+  const int64_t es = dtype == QRITA_DTYPE_F32 ? 4 : 2;
+  if (slots > kSparseCap || (slots + 1) * 4 > (int64_t)V * es) return 0;  // kept columns fit the out rows
+  return (int)slots;
+}
 
 bool is_pinned(const void *p) {
   cudaPointerAttributes a;
@@ -402,8 +452,12 @@ int qrita_topk_topp_host(const void *logits_host, int dtype, int B, int V,
   std::lock_guard<std::mutex> lock(g_host_mu);
   HostPipe *hp = nullptr;
   const size_t nc = (size_t)H.nchunks;
-  if (host_pipe_get(dev, 2 * nc + 4, hp) != cudaSuccess) return QRITA_ECUDA;
-  cudaEvent_t *landed = hp->ev.data(), *done = landed + nc, *ev0 = done + nc;
+  if (host_pipe_get(dev, 3 * nc + 4, hp) != cudaSuccess) return QRITA_ECUDA;
+  cudaEvent_t *landed = hp->ev.data(), *done = landed + nc, *ev0 = done + nc, *fetched = ev0 + 4;
+  // > 0: sparse downloads (see sparse_slots) — for a pageable out_host, where they replace the
+  // staging copy (a page-locked out_host receives the dense rows by DMA as fast as the host could fill them)
+  const int slots = is_pinned(out_host) && !getenv("QRITA_HOST_SPARSE") ? 0 : sparse_slots(B, V, dtype, k_host);
+  int32_t *kidx_d = (int32_t *)(sc + H.out), *cnt_d = kidx_d + (size_t)B * slots;
   const cudaStream_t caller = (cudaStream_t)stream;
   auto ok = [](cudaError_t e) { return e == cudaSuccess; };
   // QRITA_HOST_TRACE: timing events per chunk (uploaded / truncated / downloaded), printed to stderr
@@ -426,7 +480,42 @@ int qrita_topk_topp_host(const void *logits_host, int dtype, int B, int V,
   // Pageable buffers: the host copies each chunk into a page-locked slot (CopyPool, many threads)
   // right before its upload, and each downloaded chunk out of its slot one chunk later, so the DMA
   // of chunk c overlaps the host copies of chunks c +- 1.
-  const bool in_staged = !is_pinned(logits_host), out_staged = !is_pinned(out_host);
+  const bool in_staged = !is_pinned(logits_host), out_staged = !slots && !is_pinned(out_host);
+  if (slots) {
+    const size_t need = (size_t)B * (slots + 1) * 4;
+    if (hp->kept_host_bytes < need) {
+      if (hp->kept_host) cudaFreeHost(hp->kept_host);
+      hp->kept_host = nullptr;
+      hp->kept_host_bytes = 0;
+      if (!ok(cudaHostAlloc((void **)&hp->kept_host, need, cudaHostAllocPortable))) return QRITA_ECUDA;
+      hp->kept_host_bytes = need;
+    }
+  }
+  // sparse: the masked rows of chunk c, built on the host from the input and the kept columns
+  auto build = [&](size_t c) -> bool {
+    const size_t r0 = (size_t)H.chunks[c].first, nr = (size_t)H.chunks[c].second;
+    if (!ok(cudaEventSynchronize(fetched[c]))) return false;
+    const int32_t *kh = hp->kept_host, *ch = hp->kept_host + (size_t)B * slots;
+    CopyPool::get().parallel_for(nr, [&](size_t i) {
+      const size_t r = r0 + i;
+      const int32_t n = std::max(0, std::min(ch[r], slots));  // invalid rows: whatever came back
+      const int32_t *cols = kh + r * (size_t)slots;
+      if (es == 4) {
+        uint32_t *o = (uint32_t *)((uint8_t *)out_host + r * row_bytes);
+        const uint32_t *x = (const uint32_t *)((const uint8_t *)logits_host + r * row_bytes);
+        std::fill_n(o, (size_t)V, 0xff800000u);
+        for (int32_t j = 0; j < n; ++j)
+          if ((uint32_t)cols[j] < (uint32_t)V) o[cols[j]] = x[cols[j]];
+      } else {
+        uint16_t *o = (uint16_t *)((uint8_t *)out_host + r * row_bytes);
+        const uint16_t *x = (const uint16_t *)((const uint8_t *)logits_host + r * row_bytes);
+        std::fill_n(o, (size_t)V, (uint16_t)0xff80u);
+        for (int32_t j = 0; j < n; ++j)
+          if ((uint32_t)cols[j] < (uint32_t)V) o[cols[j]] = x[cols[j]];
+      }
+    });
+    return true;
+  };
   if ((in_staged || out_staged) &&
       host_stage_reserve(hp, (size_t)H.chunks[0].second * row_bytes) != cudaSuccess)
     return QRITA_ECUDA;
@@ -459,16 +548,36 @@ int qrita_topk_topp_host(const void *logits_host, int dtype, int B, int V,
     const size_t r0 = (size_t)H.chunks[c].first, nr = (size_t)H.chunks[c].second;
     if (in_staged && !upload(c)) return QRITA_ECUDA;
     if (!ok(cudaStreamWaitEvent(hp->comp, landed[c], 0))) return QRITA_ECUDA;
-    const int rc = topk_topp_impl(sc + H.in + r0 * row_bytes, V, dtype, (int)nr, V,
-                                  (const int64_t *)(sc + H.k) + r0, (const double *)(sc + H.p) + r0,
-                                  sc + H.out + r0 * row_bytes, V, kept_count ? kept_count + r0 : NULL,
-                                  metrics ? metrics + r0 : NULL, sc + c * H.ws_each, H.ws_each, flags, sample_size,
-                                  (qrita_stream_t)hp->comp, NULL, NULL, (int32_t *)(sc + H.st) + r0,
-                                  (int32_t *)(sc + H.nf) + r0);
+    const int rc = slots
+        ? topk_topp_impl(sc + H.in + r0 * row_bytes, V, dtype, (int)nr, V, (const int64_t *)(sc + H.k) + r0,
+                         (const double *)(sc + H.p) + r0, NULL, V, cnt_d + r0, metrics ? metrics + r0 : NULL,
+                         sc + c * H.ws_each, H.ws_each, flags, sample_size, (qrita_stream_t)hp->comp, NULL, NULL,
+                         (int32_t *)(sc + H.st) + r0, (int32_t *)(sc + H.nf) + r0, kidx_d + r0 * (size_t)slots,
+                         slots)
+        : topk_topp_impl(sc + H.in + r0 * row_bytes, V, dtype, (int)nr, V, (const int64_t *)(sc + H.k) + r0,
+                         (const double *)(sc + H.p) + r0, sc + H.out + r0 * row_bytes, V,
+                         kept_count ? kept_count + r0 : NULL, metrics ? metrics + r0 : NULL, sc + c * H.ws_each,
+                         H.ws_each, flags, sample_size, (qrita_stream_t)hp->comp, NULL, NULL,
+                         (int32_t *)(sc + H.st) + r0, (int32_t *)(sc + H.nf) + r0);
     if (rc != QRITA_OK) return rc;
     if (trace) cudaEventRecord(tr[nc + c], hp->comp);
     if (!ok(cudaEventRecord(done[c], hp->comp)) || !ok(cudaStreamWaitEvent(hp->down, done[c], 0)))
       return QRITA_ECUDA;
+    if (slots) {
+      // the chunk's kept columns and counts; the host builds chunk c - 1 meanwhile
+      if (!ok(cudaMemcpyAsync(hp->kept_host + r0 * (size_t)slots, kidx_d + r0 * (size_t)slots,
+                              nr * (size_t)slots * 4, cudaMemcpyDeviceToHost, hp->down)) ||
+          !ok(cudaMemcpyAsync(hp->kept_host + (size_t)B * slots + r0, cnt_d + r0, nr * 4, cudaMemcpyDeviceToHost,
+                              hp->down)) ||
+          !ok(cudaEventRecord(fetched[c], hp->down)))
+        return QRITA_ECUDA;
+      if (kept_count && !ok(cudaMemcpyAsync(kept_count + r0, cnt_d + r0, nr * 4, cudaMemcpyDeviceToDevice,
+                                            hp->down)))
+        return QRITA_ECUDA;
+      if (trace) cudaEventRecord(tr[2 * nc + c], hp->down);
+      if (c > 0 && !build(c - 1)) return QRITA_ECUDA;
+      continue;
+    }
     if (out_staged) {
       if (!ok(cudaMemcpyAsync(hp->stage_out[c & 1], sc + H.out + r0 * row_bytes, nr * row_bytes,
                               cudaMemcpyDeviceToHost, hp->down)) ||
@@ -482,6 +591,7 @@ int qrita_topk_topp_host(const void *logits_host, int dtype, int B, int V,
     if (trace) cudaEventRecord(tr[2 * nc + c], hp->down);
   }
   if (out_staged && !drain(nc - 1)) return QRITA_ECUDA;
+  if (slots && !build(nc - 1)) return QRITA_ECUDA;
   if (trace) {
     cudaDeviceSynchronize();
     for (size_t c = 0; c < nc; ++c) {
@@ -499,6 +609,14 @@ int qrita_topk_topp_host(const void *logits_host, int dtype, int B, int V,
       !ok(cudaStreamWaitEvent(caller, ev0[2], 0)) || !ok(cudaStreamWaitEvent(caller, ev0[3], 0)))
     return QRITA_ECUDA;
   return QRITA_OK;
+}
+
+int64_t qrita_host_download_bytes(int B, int V, int dtype, const int64_t *k_host, const void *out_host) {
+  if (B < 1 || V < 1 || !k_host) return -1;
+  const int slots = out_host && is_pinned(out_host) && !getenv("QRITA_HOST_SPARSE") ? 0
+                                                                                     : sparse_slots(B, V, dtype, k_host);
+  const int64_t es = dtype == QRITA_DTYPE_F32 ? 4 : 2;
+  return slots ? (int64_t)B * (slots + 1) * 4 : (int64_t)B * V * es;
 }
 
 int qrita_get_status_host(const void *scratch, int B, int V, int dtype, int chunk_rows, int *row, int *col,

@@ -440,3 +440,35 @@ def test_kept_indices_paths(cuda_device):
                 got = _idx_sets(kidx.cpu().numpy(), kc.cpu().numpy())
                 for r in range(8):
                     assert np.array_equal(got[r], want[r]), (v, dtype, fl, r, k[r], p[r])
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+def test_host_sparse_download_pageable_out(cuda_device, dtype):
+    """Pageable output + every row top-k (k <= 4096): only kept columns come back and the host builds
+    the masked rows from its input copy — bit-identical to the dense download (QRITA_HOST_DENSE)
+    and to the oracle; a top-p-only row in the batch switches the call to dense downloads."""
+    import ctypes
+    from paper_2602_01518_b200 import _native as N
+    x, k, p, _, trip, _ = G.config("cfg2")
+    n = 40
+    xh = torch.from_numpy(np.ascontiguousarray(x[:n])).to(dtype)
+    kh, ph = torch.from_numpy(k[:n]).clone(), torch.from_numpy(p[:n])
+    out = torch.empty_like(xh)  # pageable
+    lib = N.load()
+    es = 4 if dtype == torch.float32 else 2
+    sparse_bytes = lib.qrita_host_download_bytes(n, x.shape[1], 0 if es == 4 else 1,
+                                                 ctypes.c_void_p(kh.data_ptr()), ctypes.c_void_p(out.data_ptr()))
+    assert 0 < sparse_bytes < n * x.shape[1] * es
+    Q.ops.topk_topp_host(xh, kh, ph, out=out, chunk_bytes=9 * x.shape[1] * es)
+    xs = xh.float().numpy()
+    for r in range(n):
+        ref = oracle_keep_row(xs[r], int(kh[r]), float(ph[r]))
+        got = out[r].float().numpy()
+        assert np.array_equal(np.isfinite(got), ref), r
+        assert np.array_equal(got[ref], xs[r][ref]), r
+    kh[7] = x.shape[1]                                # a top-p-only row: dense downloads
+    assert lib.qrita_host_download_bytes(n, x.shape[1], 0 if es == 4 else 1, ctypes.c_void_p(kh.data_ptr()),
+                                         ctypes.c_void_p(out.data_ptr())) == n * x.shape[1] * es
+    Q.ops.topk_topp_host(xh, kh, ph, out=out)
+    ref = oracle_keep_row(xs[7], int(kh[7]), float(ph[7]))
+    assert np.array_equal(np.isfinite(out[7].float().numpy()), ref)
