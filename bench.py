@@ -632,15 +632,20 @@ def bench_lmhead(args, rank: int, world: int, dev):
     ms_unfused = sharded_max(timed(unfused, max(3, args.steps // 2)), world, dev)
     ms_gemm = sharded_max(timed(lambda: lm_head_logits(h, w, out=logits), max(3, args.steps // 2)), world, dev)
     ms_cublas = sharded_max(timed(lambda: h @ w.T, max(3, args.steps // 2)), world, dev)
-    # end to end: hidden states from pinned host memory in, kept columns + counts back to the host
+    # end to end: hidden states from pinned host memory in; the kept columns (compact lists,
+    # k_cap = 1024), their logits and the counts back to the host
     h_host = h.cpu().pin_memory()
-    kidx_host = torch.empty(b, v, dtype=torch.int32).pin_memory()
+    kcap = 1024
+    kidx_host = torch.empty(b, kcap, dtype=torch.int32).pin_memory()
+    kval_host = torch.empty(b, kcap, dtype=torch.float32).pin_memory()
     kc_host = torch.empty(b, dtype=torch.int32).pin_memory()
 
     def e2e():
         hd = h_host.to(dev, non_blocking=True)
-        _, kidx, kc = lm_head_topk_topp(hd, w, k, p)
+        lg, kidx, kc = lm_head_topk_topp(hd, w, k, p, k_cap=kcap)
+        kval = torch.gather(lg, 1, kidx.clamp(0, v - 1).long())  # entries past kc[r] are ignored
         kidx_host.copy_(kidx, non_blocking=True)
+        kval_host.copy_(kval, non_blocking=True)
         kc_host.copy_(kc, non_blocking=True)
     ms_e2e = sharded_max(timed(e2e, max(3, args.steps // 2)), world, dev)
     flops = 2.0 * b * v * d
@@ -662,7 +667,9 @@ def bench_lmhead(args, rank: int, world: int, dev):
                      "kernel": "whole qrita_lmhead_topk_topp call (GEMM + epilogue + row tails)"},
         "unfused_ms": ms_unfused, "gemm_only_ms": ms_gemm, "cublas_bf16_matmul_ms": ms_cublas,
         "e2e": {"value": world * b / (ms_e2e / 1e3), "unit": "rows/s", "h2d_bytes_per_step": b * d * 2,
-                "d2h_bytes_per_step": b * v * 4 + b * 4, "ms_per_step": ms_e2e},
+                "d2h_bytes_per_step": b * kcap * 8 + b * 4, "ms_per_step": ms_e2e,
+                "api": "lm_head_topk_topp(hidden from pinned host memory, k_cap=1024) -> kept columns, their "
+                       "logits and counts to pinned host memory"},
         "clocks": clk.summary(),
         "gpu_launches": 2 * args.steps,  # lmh_gemm, qrita_tail (plus a counter memset)
     }

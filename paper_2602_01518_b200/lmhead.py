@@ -55,13 +55,15 @@ def lm_head_logits(hidden: torch.Tensor, weight: torch.Tensor, *, out: Optional[
 
 def lm_head_topk_topp(hidden: torch.Tensor, weight: torch.Tensor, k: Union[int, torch.Tensor],
                       p: Union[float, torch.Tensor], *, flags: Optional[TruncFlags] = None,
-                      metrics: Optional[torch.Tensor] = None, check: bool = False,
+                      metrics: Optional[torch.Tensor] = None, check: bool = False, k_cap: Optional[int] = None,
                       stream: Optional[torch.cuda.Stream] = None
                       ) -> Tuple[torch.Tensor, torch.Tensor, torch.Tensor]:
     """LM head + exact Top-k / Top-p in one pipeline.  Returns (logits fp32 [B, V], kept_idx int32
-    [B, V], kept_count int32 [B]); row r keeps logits[r, kept_idx[r, :kept_count[r]]] (unordered) —
-    the same set topk_topp_indices(logits, k, p) returns.  Stream-ordered; check=True synchronises and
-    raises the reference's ValueError for invalid rows."""
+    [B, V] — or [B, k_cap] with k_cap —, kept_count int32 [B]); row r keeps
+    logits[r, kept_idx[r, :kept_count[r]]] (unordered), the set topk_topp_indices(logits, k, p)
+    returns.  k_cap: compact kept lists for batches whose rows are all top-k rows with k <= k_cap < V
+    (checked, one synchronisation).  Stream-ordered; check=True synchronises and raises the reference's
+    ValueError for invalid rows."""
     b, v, d = _check(hidden, weight)
     dev = hidden.device
     fl = (flags or TruncFlags()).bits()
@@ -73,13 +75,20 @@ def lm_head_topk_topp(hidden: torch.Tensor, weight: torch.Tensor, k: Union[int, 
         kt = _per_row(k, b, torch.int64, dev, "k")
         pt = _per_row(p, b, torch.float64, dev, "p")
         logits = torch.empty((b, v), dtype=torch.float32, device=dev)
-        kept_idx = torch.empty((b, v), dtype=torch.int32, device=dev)
+        ld_idx = v
+        if k_cap is not None:
+            kmax = int(kt.max().item())
+            if not (1 <= int(kt.min().item()) and kmax <= int(k_cap) < v):
+                raise ValueError(f"k_cap={k_cap} needs every row to be a top-k row with k <= k_cap < V "
+                                 f"(max k {kmax}, V {v})")
+            ld_idx = int(k_cap)
+        kept_idx = torch.empty((b, ld_idx), dtype=torch.int32, device=dev)
         kept_count = torch.empty((b,), dtype=torch.int32, device=dev)
         ws_ptr, ws_bytes = ws.get(need, st)
         rc = lib.qrita_lmhead_topk_topp(
             ctypes.c_void_p(hidden.data_ptr()), hidden.stride(0), ctypes.c_void_p(weight.data_ptr()),
             weight.stride(0), b, v, d, ctypes.c_void_p(kt.data_ptr()), ctypes.c_void_p(pt.data_ptr()),
-            ctypes.c_void_p(logits.data_ptr()), v, ctypes.c_void_p(kept_idx.data_ptr()), v,
+            ctypes.c_void_p(logits.data_ptr()), v, ctypes.c_void_p(kept_idx.data_ptr()), ld_idx,
             ctypes.c_void_p(kept_count.data_ptr()), ctypes.c_void_p(metrics.data_ptr() if metrics is not None else 0),
             ctypes.c_void_p(ws_ptr), ws_bytes, fl, ctypes.c_void_p(st.cuda_stream))
         if rc != N.OK:

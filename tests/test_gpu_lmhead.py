@@ -96,3 +96,15 @@ def test_fused_metrics_match_the_truncation_path(cuda_device):
     for r in range(b):
         for key in ("trunc_hit", "outlier_count", "fallback_used", "kept_count"):
             assert got[r][key] == want[r][key], (r, key, got[r][key], want[r][key])
+
+
+def test_fused_compact_kept_lists(cuda_device):
+    h, w = _operands(12, 9000, 128, 5)
+    k = torch.tensor([5, 1000, 64, 999, 1, 300, 17, 1000, 2, 800, 50, 1000])
+    p = torch.full((12,), 0.9, dtype=torch.float64)
+    logits, kidx, kc = lm_head_topk_topp(h, w, k, p, k_cap=1000)
+    assert kidx.shape == (12, 1000)
+    want = _kept_sets(*Q.topk_topp_indices(logits, k.cuda(), p.cuda()))
+    assert all(np.array_equal(a, c) for a, c in zip(_kept_sets(kidx, kc), want))
+    with pytest.raises(ValueError):
+        lm_head_topk_topp(h, w, k, p, k_cap=999)
