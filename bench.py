@@ -465,9 +465,11 @@ def main():
                 tt.append(e0.elapsed_time(e1))
         h2d = x_host.numel() * x_host.element_size() + b * 16
         # what the host pipeline downloads: the masked rows, or (sparse form, every row top-k with
-        # k <= 4096) each row's kept columns + counts; plus the status words
+        # k <= 4096) each row's kept columns + counts, the host building the masked rows; plus the
+        # status words
         d2h = int(N.load().qrita_host_download_bytes(b, v, 0 if dtype == "f32" else 1,
                                                      ctypes.c_void_p(k_host.data_ptr()),
+                                                     ctypes.c_void_p(x_host.data_ptr()),
                                                      ctypes.c_void_p(o_host.data_ptr()))) + b * 8
         e2e_ms = sharded_max(statistics.mean(tt), world, dev)
         line["e2e"] = {"value": total_rows / (e2e_ms / 1e3), "unit": "rows/s", "h2d_bytes_per_step": h2d,

@@ -148,14 +148,16 @@ int qrita_topk_topp_ex(const void *logits, int64_t ld_in, int dtype, int B, int 
  * needed).  The work is ordered after everything already enqueued on `stream`, and `stream` waits
  * for all of it: synchronise `stream` before reading `out`.  kept_count / metrics: DEVICE or NULL.
  * Invalid rows are reported by qrita_get_status_host.
- * Sparse downloads: with a pageable out_host and every row 1 <= k < V, k <= 4096 (top-k active), the
- * kernels write each row's kept columns instead of its masked row, only those (and the counts) cross
- * PCIe, and host threads build the masked rows from logits_host (-inf fill, kept entries copied:
- * bit-identical) — no staging copy of the output.  qrita_host_download_bytes(B, V, dtype, k_host,
- * out_host) gives the bytes a call downloads (QRITA_HOST_DENSE=1 disables the sparse form).
+ * Sparse downloads: when every row has 1 <= k < V, k <= 4096 (top-k active) — and unless a pageable
+ * logits_host meets a page-locked out_host — the kernels write each row's kept columns instead of its
+ * masked row, only those (and the counts) cross PCIe, and host threads build the masked rows from
+ * logits_host (-inf fill, kept entries copied: bit-identical); the call then returns with out_host
+ * complete.  qrita_host_download_bytes(B, V, dtype, k_host, logits_host, out_host) gives the bytes a
+ * call downloads (QRITA_HOST_DENSE=1 / QRITA_HOST_SPARSE=1 force either form).
  */
 size_t qrita_host_scratch_bytes(int B, int V, int dtype, int chunk_rows);
-int64_t qrita_host_download_bytes(int B, int V, int dtype, const int64_t *k_host, const void *out_host);
+int64_t qrita_host_download_bytes(int B, int V, int dtype, const int64_t *k_host, const void *logits_host,
+                                  const void *out_host);
 int qrita_topk_topp_host(const void *logits_host, int dtype, int B, int V,
                          const int64_t *k_host, const double *p_host, void *out_host,
                          int32_t *kept_count, qrita_row_metrics *metrics,

@@ -120,7 +120,7 @@ def load() -> ctypes.CDLL:
     lib.qrita_sigma_table.restype = i32
     lib.qrita_row_stats.argtypes = [vp, i64, i32, i32, i32, i32, vp, vp]
     lib.qrita_row_stats.restype = i32
-    lib.qrita_host_download_bytes.argtypes = [i32, i32, i32, vp, vp]
+    lib.qrita_host_download_bytes.argtypes = [i32, i32, i32, vp, vp, vp]
     lib.qrita_host_download_bytes.restype = i64
     lib.qrita_lmhead_logits.argtypes = [vp, i64, vp, i64, i32, i32, i32, vp, i64, vp]
     lib.qrita_lmhead_logits.restype = i32

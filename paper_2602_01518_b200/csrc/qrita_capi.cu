@@ -267,7 +267,6 @@ class CopyPool {
 // the batch is not eligible.
 constexpr int64_t kSparseCap = 4096;
 int sparse_slots(int B, int V, int dtype, const int64_t *k_host) {
-  if (getenv("QRITA_HOST_DENSE")) return 0;
   int64_t kmax = 0;
   for (int r = 0; r < B; ++r) {
     const int64_t k = k_host[r];
@@ -287,6 +286,17 @@ bool is_pinned(const void *p) {
     return false;
   }
   return a.type == cudaMemoryTypeHost;
+}
+
+// Sparse or dense downloads for a host-buffer call (measured, tools/e2e_sparse_sweep.py /
+// tools/e2e_pageable.py): sparse whenever eligible, except for a pageable input with a page-locked
+// output, where the host threads are busy staging the input and the DMA delivers the dense rows
+// faster than they could build them.
+int host_slots(int B, int V, int dtype, const int64_t *k_host, const void *in_host, const void *out_host) {
+  if (getenv("QRITA_HOST_DENSE")) return 0;
+  const bool force = getenv("QRITA_HOST_SPARSE") != nullptr;
+  if (!force && in_host && out_host && !is_pinned(in_host) && is_pinned(out_host)) return 0;
+  return sparse_slots(B, V, dtype, k_host);
 }
 
 }  // namespace
@@ -454,9 +464,7 @@ int qrita_topk_topp_host(const void *logits_host, int dtype, int B, int V,
   const size_t nc = (size_t)H.nchunks;
   if (host_pipe_get(dev, 3 * nc + 4, hp) != cudaSuccess) return QRITA_ECUDA;
   cudaEvent_t *landed = hp->ev.data(), *done = landed + nc, *ev0 = done + nc, *fetched = ev0 + 4;
-  // > 0: sparse downloads (see sparse_slots) — for a pageable out_host, where they replace the
-  // staging copy (a page-locked out_host receives the dense rows by DMA as fast as the host could fill them)
-  const int slots = is_pinned(out_host) && !getenv("QRITA_HOST_SPARSE") ? 0 : sparse_slots(B, V, dtype, k_host);
+  const int slots = host_slots(B, V, dtype, k_host, logits_host, out_host);  // > 0: sparse downloads
   int32_t *kidx_d = (int32_t *)(sc + H.out), *cnt_d = kidx_d + (size_t)B * slots;
   const cudaStream_t caller = (cudaStream_t)stream;
   auto ok = [](cudaError_t e) { return e == cudaSuccess; };
@@ -611,10 +619,10 @@ int qrita_topk_topp_host(const void *logits_host, int dtype, int B, int V,
   return QRITA_OK;
 }
 
-int64_t qrita_host_download_bytes(int B, int V, int dtype, const int64_t *k_host, const void *out_host) {
+int64_t qrita_host_download_bytes(int B, int V, int dtype, const int64_t *k_host, const void *logits_host,
+                                  const void *out_host) {
   if (B < 1 || V < 1 || !k_host) return -1;
-  const int slots = out_host && is_pinned(out_host) && !getenv("QRITA_HOST_SPARSE") ? 0
-                                                                                     : sparse_slots(B, V, dtype, k_host);
+  const int slots = host_slots(B, V, dtype, k_host, logits_host, out_host);
   const int64_t es = dtype == QRITA_DTYPE_F32 ? 4 : 2;
   return slots ? (int64_t)B * (slots + 1) * 4 : (int64_t)B * V * es;
 }

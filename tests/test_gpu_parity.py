@@ -456,8 +456,8 @@ def test_host_sparse_download_pageable_out(cuda_device, dtype):
     out = torch.empty_like(xh)  # pageable
     lib = N.load()
     es = 4 if dtype == torch.float32 else 2
-    sparse_bytes = lib.qrita_host_download_bytes(n, x.shape[1], 0 if es == 4 else 1,
-                                                 ctypes.c_void_p(kh.data_ptr()), ctypes.c_void_p(out.data_ptr()))
+    sparse_bytes = lib.qrita_host_download_bytes(n, x.shape[1], 0 if es == 4 else 1, ctypes.c_void_p(kh.data_ptr()),
+                                                 ctypes.c_void_p(xh.data_ptr()), ctypes.c_void_p(out.data_ptr()))
     assert 0 < sparse_bytes < n * x.shape[1] * es
     Q.ops.topk_topp_host(xh, kh, ph, out=out, chunk_bytes=9 * x.shape[1] * es)
     xs = xh.float().numpy()
@@ -468,6 +468,7 @@ def test_host_sparse_download_pageable_out(cuda_device, dtype):
         assert np.array_equal(got[ref], xs[r][ref]), r
     kh[7] = x.shape[1]                                # a top-p-only row: dense downloads
     assert lib.qrita_host_download_bytes(n, x.shape[1], 0 if es == 4 else 1, ctypes.c_void_p(kh.data_ptr()),
+                                         ctypes.c_void_p(xh.data_ptr()),
                                          ctypes.c_void_p(out.data_ptr())) == n * x.shape[1] * es
     Q.ops.topk_topp_host(xh, kh, ph, out=out)
     ref = oracle_keep_row(xs[7], int(kh[7]), float(ph[7]))
