@@ -170,7 +170,7 @@ class CopyPool {
     static CopyPool *pool = new CopyPool();  // never destroyed: its threads end with the process
     return *pool;
   }
-  // fn(0 .. n-1) over the pool (items claimed one at a time; the caller is one of the workers)
+  // fn(0 .. n-1) over every thread of the pool (items claimed one at a time; the caller helps)
   void parallel_for(size_t n, const std::function<void(size_t)> &fn) {
     if (n < 2 || nthreads_ == 0) {
       for (size_t i = 0; i < n; ++i) fn(i);
@@ -182,6 +182,7 @@ class CopyPool {
       fn_ = &fn;
       items_ = n;
       next_.store(0);
+      limit_ = nthreads_;
       active_ = nthreads_;
       ++gen_;
     }
@@ -191,8 +192,9 @@ class CopyPool {
     cv_done_.wait(lk, [&] { return active_ == 0; });
     fn_ = nullptr;
   }
+  // memcpy over `copiers_` threads (more compete with the DMA for host memory bandwidth)
   void copy(void *d, const void *s, size_t n) {
-    if (n < (1u << 20) || nthreads_ == 0) {
+    if (n < (1u << 20) || copiers_ == 0) {
       memcpy(d, s, n);
       return;
     }
@@ -203,11 +205,12 @@ class CopyPool {
       dst_ = (uint8_t *)d;
       src_ = (const uint8_t *)s;
       bytes_ = n;
-      size_t piece = n / (size_t)(4 * (nthreads_ + 1));
+      size_t piece = n / (size_t)(4 * (copiers_ + 1));
       piece = std::max<size_t>(piece, 256u << 10);
       piece_ = (piece + 4095) & ~(size_t)4095;
       next_.store(0);
-      active_ = nthreads_;
+      limit_ = copiers_;
+      active_ = copiers_;
       ++gen_;
     }
     cv_work_.notify_all();
@@ -218,13 +221,17 @@ class CopyPool {
 
  private:
   CopyPool() {
-    // half the hardware threads, at most 8: measured best on the 16-core B200 host (cfg2 run_batch
-    // 5.0 ms with 8 copiers vs 6.5 ms with 16, tools/e2e_pageable.py)
-    int n = std::min(8, std::max(1, (int)std::thread::hardware_concurrency() / 2));
-    if (const char *ev = getenv("QRITA_HOST_COPY_THREADS")) n = atoi(ev);
-    n = std::max(0, std::min(n, 32) - 1);  // the caller is one of the copiers
-    nthreads_ = n;
-    for (int i = 0; i < n; ++i) std::thread([this] { worker(); }).detach();
+    // copies: half the hardware threads, at most 8 — measured best on the 16-core B200 host (cfg2
+    // run_batch 5.0 ms with 8 copiers vs 6.5 ms with 16, tools/e2e_pageable.py); host-built rows of
+    // sparse downloads: every hardware thread (2.98 ms with 8, 2.77-2.83 with 12-16,
+    // tools/e2e_sparse_sweep.py)
+    const int hw = std::max(1, (int)std::thread::hardware_concurrency());
+    int c = std::min(8, std::max(1, hw / 2)), t = hw;
+    if (const char *ev = getenv("QRITA_HOST_COPY_THREADS")) c = atoi(ev);
+    if (const char *ev = getenv("QRITA_HOST_BUILD_THREADS")) t = atoi(ev);
+    copiers_ = std::max(0, std::min(c, 32) - 1);  // the caller is one of them
+    nthreads_ = std::max(copiers_, std::max(0, std::min(t, 32) - 1));
+    for (int i = 0; i < nthreads_; ++i) std::thread([this, i] { worker(i); }).detach();
   }
   void run_pieces() {
     if (fn_) {
@@ -237,12 +244,13 @@ class CopyPool {
       memcpy(dst_ + off, src_ + off, std::min(piece_, bytes_ - off));
     }
   }
-  void worker() {
+  void worker(int id) {
     uint64_t seen = 0;
     std::unique_lock<std::mutex> lk(mu_);
     for (;;) {
       cv_work_.wait(lk, [&] { return gen_ != seen; });
       seen = gen_;
+      if (id >= limit_) continue;  // not part of this job
       lk.unlock();
       run_pieces();
       lk.lock();
@@ -251,7 +259,7 @@ class CopyPool {
   }
   std::mutex call_mu_, mu_;
   std::condition_variable cv_work_, cv_done_;
-  int nthreads_ = 0, active_ = 0;
+  int nthreads_ = 0, copiers_ = 0, limit_ = 0, active_ = 0;
   uint64_t gen_ = 0;
   uint8_t *dst_ = nullptr;
   const uint8_t *src_ = nullptr;
