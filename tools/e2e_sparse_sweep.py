@@ -1,12 +1,11 @@
-"""cfg2 end to end through Q.ops.topk_topp_host (pinned in / pinned out): dense downloads vs sparse
-(kept columns, host-built rows; QRITA_HOST_SPARSE=1) over chunk sizes."""
+"""cfg2 end to end through Q.ops.topk_topp_host (pinned in / pinned out): dense downloads
+(QRITA_HOST_DENSE=1) vs sparse (kept columns, host-built rows; the default here) over chunk sizes."""
 import sys, os, statistics, subprocess
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 if len(sys.argv) < 2:
     for mode in ("dense", "sparse"):
         env = dict(os.environ)
-        if mode == "sparse":
-            env["QRITA_HOST_SPARSE"] = "1"
+        env["QRITA_HOST_DENSE" if mode == "dense" else "QRITA_HOST_SPARSE"] = "1"
         subprocess.run([sys.executable, __file__, mode], env=env)
     sys.exit(0)
 import torch
