@@ -174,9 +174,10 @@ int qrita_get_status_host(const void *scratch, int B, int V, int dtype, int chun
  * (shards contiguous, offsets increasing with rank) and receives its shard of the UNSHARDED answer,
  * bit-exact.  Only per-row partials cross ranks (include: what is exchanged, bytes per row):
  *   1. local top-min(k, V_shard) candidates (top-p-only rows: the local max), one all-gather of
- *      (order key, global column) pairs, sorted by column: <= 8 * k_cap bytes per row per rank;
- *      every rank resolves top-k + top-p on the gathered candidates with the single-GPU kernels
- *      (global stable order, full-row max and survivor normaliser all live in that set);
+ *      (order key, global column) pairs, each rank's list sorted by (value desc, column asc):
+ *      <= 8 * k_cap bytes per row per rank; every rank merges the lists into the global top-k and
+ *      resolves top-p over it (global stable order, full-row max and survivor normaliser all live
+ *      in that set);
  *   2. top-p-only rows only: the exact normaliser (fixed-point limbs, integer all-reduce SUM: exact
  *      and order-independent), then 4 (bf16) / 8 (fp32) radix passes, each an all-reduce SUM of 16
  *      (count, exact mass) partials per row, then one all-reduce of the per-rank boundary-tie counts

@@ -9,12 +9,16 @@
 //  top-k / top-k+top-p rows (k < V):
 //    tp_prep  -> k_loc = min(k, Vr)             (top-p-only rows: k_loc = 1, i.e. the local max)
 //    local top-k_loc with the single-GPU kernels (index-only output, one read of the shard)
-//    tp_pack  -> (order key, global column) pairs sorted by column, padded to kmax per row
+//    tp_pack_sorted -> (order key, global column) pairs sorted by (value desc, column asc), padded
+//                 to kmax per row (already in order when the shard call's bin-sort emitted them so)
 //    all_gather                                   <= 8 * kmax bytes per row per rank
-//    tp_merge -> candidate rows [B, world*kmax] in global column order (rank order = index order)
-//    the single-GPU kernels on the candidate rows with the ORIGINAL k and p: the global top-k is a
-//    subset of the union of the local top-k sets, and the full-row max (the global top-1), the
-//    survivor normaliser and the nucleus all depend on that set only
+//    tp_merge_resolve -> the ranks' sorted lists merged (bitonic merge tree, or binary-search ranks)
+//                 into the global top-k in order, then the exact normaliser / nucleus over it with
+//                 the ORIGINAL k and p: the global top-k is a subset of the union of the local top-k
+//                 sets, and the full-row max (the global top-1), the survivor normaliser and the
+//                 nucleus all depend on that set only
+//    (candidate rows wider than kSmallW: tp_pack by column, tp_merge into column-ordered rows, and
+//    the single-GPU kernels on them)
 //  top-p-only rows (k == V, p < 1), which need the whole row:
 //    global max   = max of the gathered local maxima
 //    tp_denom -> D = sum_i exp(z_i - m) as exact 192-bit fixed point, 4 limbs of 48 bits
