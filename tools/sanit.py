@@ -96,6 +96,16 @@ def main(case):
         for i in range(x.shape[0]):
             got[i, idx[i, :cnt[i]]] = x[i, idx[i, :cnt[i]]]
         check(x, got, k, p, case)
+    elif case == "hostsparse":  # every row top-k: sparse downloads, host-built rows (pinned and pageable out)
+        x, k, p = mixed(96, 8192, 11)
+        k = np.minimum(k, 1000)
+        for pin in (False, True):
+            xh = torch.from_numpy(x)
+            oh = torch.empty_like(xh)
+            if pin:
+                xh, oh = xh.pin_memory(), oh.pin_memory()
+            out = Q.ops.topk_topp_host(xh, torch.from_numpy(k), torch.from_numpy(p), out=oh)
+            check(x, out.numpy(), k, p, f"{case} pinned={pin}")
     elif case == "host":
         x, k, p = mixed(200, 8192, 9)
         out = Q.topk_topp(torch.from_numpy(x), torch.from_numpy(k), torch.from_numpy(p))
