@@ -508,7 +508,18 @@ int qrita_topk_topp_host(const void *logits_host, int dtype, int B, int V,
     }
   }
   // sparse: the masked rows of chunk c, built on the host from the input and the kept columns
-  auto build = [&](size_t c) -> bool {
+  // -inf background of chunk c's rows: needs nothing from the GPU, so it runs while the chunk is
+  // still uploading / being truncated
+  auto fill = [&](size_t c) {
+    const size_t r0 = (size_t)H.chunks[c].first, nr = (size_t)H.chunks[c].second;
+    CopyPool::get().parallel_for(nr, [&](size_t i) {
+      uint8_t *o = (uint8_t *)out_host + (r0 + i) * row_bytes;
+      if (es == 4) std::fill_n((uint32_t *)o, (size_t)V, 0xff800000u);
+      else std::fill_n((uint16_t *)o, (size_t)V, (uint16_t)0xff80u);
+    });
+  };
+  // the kept entries of chunk c, copied from the host's own logits once its kept columns are back
+  auto scatter = [&](size_t c) -> bool {
     const size_t r0 = (size_t)H.chunks[c].first, nr = (size_t)H.chunks[c].second;
     if (!ok(cudaEventSynchronize(fetched[c]))) return false;
     const int32_t *kh = hp->kept_host, *ch = hp->kept_host + (size_t)B * slots;
@@ -519,13 +530,11 @@ int qrita_topk_topp_host(const void *logits_host, int dtype, int B, int V,
       if (es == 4) {
         uint32_t *o = (uint32_t *)((uint8_t *)out_host + r * row_bytes);
         const uint32_t *x = (const uint32_t *)((const uint8_t *)logits_host + r * row_bytes);
-        std::fill_n(o, (size_t)V, 0xff800000u);
         for (int32_t j = 0; j < n; ++j)
           if ((uint32_t)cols[j] < (uint32_t)V) o[cols[j]] = x[cols[j]];
       } else {
         uint16_t *o = (uint16_t *)((uint8_t *)out_host + r * row_bytes);
         const uint16_t *x = (const uint16_t *)((const uint8_t *)logits_host + r * row_bytes);
-        std::fill_n(o, (size_t)V, (uint16_t)0xff80u);
         for (int32_t j = 0; j < n; ++j)
           if ((uint32_t)cols[j] < (uint32_t)V) o[cols[j]] = x[cols[j]];
       }
@@ -591,7 +600,8 @@ int qrita_topk_topp_host(const void *logits_host, int dtype, int B, int V,
                                             hp->down)))
         return QRITA_ECUDA;
       if (trace) cudaEventRecord(tr[2 * nc + c], hp->down);
-      if (c > 0 && !build(c - 1)) return QRITA_ECUDA;
+      fill(c);
+      if (c > 0 && !scatter(c - 1)) return QRITA_ECUDA;
       continue;
     }
     if (out_staged) {
@@ -607,7 +617,7 @@ int qrita_topk_topp_host(const void *logits_host, int dtype, int B, int V,
     if (trace) cudaEventRecord(tr[2 * nc + c], hp->down);
   }
   if (out_staged && !drain(nc - 1)) return QRITA_ECUDA;
-  if (slots && !build(nc - 1)) return QRITA_ECUDA;
+  if (slots && !scatter(nc - 1)) return QRITA_ECUDA;
   if (trace) {
     cudaDeviceSynchronize();
     for (size_t c = 0; c < nc; ++c) {
