@@ -604,17 +604,21 @@ __device__ void tail_resolve(const Params &P, int row, const RowPlan &pl, uint32
       //    the k survivors' exp(z - max) go to ev (X is no longer needed) with per-warp exact partial
       //    sums, so the normaliser needs no pass of its own
       double *ev2 = reinterpret_cast<double *>(xb);
+      // (key, ~index) composites of the binned candidates in X's free index half: one 64-bit
+      // compare per pair in the ranking below
+      unsigned long long *ck = reinterpret_cast<unsigned long long *>(xi);
+      for (int q = tid; q < (int)nC; q += kThreads)
+        ck[q] = ((unsigned long long)key_of_bits(cb[q]) << 32) | (0xffffffffu - ci[q]);
+      tsync();
       Fx se = fx_zero();
       for (int q = tid; q < (int)nC; q += kThreads) {
         const uint32_t b = cb[q], ix = ci[q], key = key_of_bits(b);
         const uint32_t bin = bin_of(key);
         const uint32_t e = he[bin], c = hcnt[bin];
         uint32_t r = 0u;
+        const unsigned long long cq = ck[q];
 #pragma unroll 4
-        for (uint32_t j = e - c; j < e; ++j) {
-          const uint32_t kj = key_of_bits(cb[j]);
-          r += (kj > key || (kj == key && ci[j] < ix)) ? 1u : 0u;
-        }
+        for (uint32_t j = e - c; j < e; ++j) r += ck[j] > cq ? 1u : 0u;
         const uint32_t d = e - c + r;
         db[d] = b; di[d] = ix;
         if (topkp && d < k) {
