@@ -360,7 +360,9 @@ def topk_topp_host(logits: torch.Tensor, k, p, *, out: Optional[torch.Tensor] = 
     """topk_topp for a host [B, V] tensor through qrita_topk_topp_host: the library copies row chunks
     of ~chunk_bytes in, truncates each as soon as it has landed and copies it back, on three streams
     of its own, so both PCIe directions stay busy and overlap the kernels.  Pinned host memory gives
-    asynchronous copies; pageable memory works, with the copies staged synchronously by CUDA.
+    asynchronous copies; pageable memory is staged through library-owned page-locked slots.  When
+    every row is a top-k row (k < V, k <= 4096) only the kept columns come back and host threads
+    build the masked rows from the input (bit-identical; not for a pageable input with a pinned out).
     Returns the masked logits as a host tensor (`out` when given); the call returns with the result in
     host memory.  kept_count / metrics, if given, are CUDA tensors.  check=True raises the
     reference's ValueError for invalid rows."""
