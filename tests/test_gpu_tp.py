@@ -82,6 +82,20 @@ def test_wide_candidate_rows(cuda_device, world):
     _check(x, out.cpu().numpy(), want, f"wide world={world}")
 
 
+def test_k_above_shard_width(cuda_device):
+    """k larger than a shard (every rank sends its whole shard): the merge resolve's binary-search
+    rank path instead of the merge tree (k exceeds the per-rank list slots)."""
+    rng = np.random.default_rng(31)
+    b, v = 10, 2000
+    x = rng.normal(0, 1, (b, v)).astype(np.float32)
+    x[6:] = np.round(x[6:] * 4) / 4                   # ties across shards
+    k = np.array([1000, 400, 1999, 251, 600, 900, 1000, 333, 1500, 260], dtype=np.int64)
+    p = np.array([0.9, 1.0, 0.95, 0.5, 0.99, 1.0, 0.8, 0.7, 1.0, 0.6])
+    want, _ = oracle_batch(x, k, p)
+    out = simulate_tp(torch.from_numpy(x).cuda(), torch.from_numpy(k).cuda(), torch.from_numpy(p).cuda(), world=8)
+    _check(x, out.cpu().numpy(), want, "k above shard width")
+
+
 def test_cfg3_rows_topp_only_bf16_tp4(cuda_device):
     x, k, p, _, trip, _ = G.config("cfg3")
     rows = slice(0, 8)
