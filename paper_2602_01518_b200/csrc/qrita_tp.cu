@@ -467,7 +467,9 @@ __global__ void __launch_bounds__(kT) tp_write(const T *logits, int64_t ld_in, T
                                               const int32_t *kidx_c, const int32_t *kc_c, int W,
                                               const uint32_t *qbuf, int rank, int world, int32_t *kept_count,
                                               int32_t *status, const int32_t *tst, int sh, int bg_done,
-                                              const int32_t *kidx_s, const int32_t *kc_s, int kmax) {
+                                              const int32_t *kidx_s, const int32_t *kc_s, int kmax,
+                                              const unsigned long long *bnd, const uint32_t *send, int B4,
+                                              int B) {
   extern __shared__ uint32_t bm[];
   __shared__ uint32_t buf[kT / 32];
   __shared__ uint32_t nkept;
@@ -481,7 +483,21 @@ __global__ void __launch_bounds__(kT) tp_write(const T *logits, int64_t ld_in, T
   T *o = out + (size_t)r * ld_out;
   const T ninf = Elem<T>::neg_inf();
   uint32_t kept = 0u;
-  if (R.mode == MODE_TOPK || R.mode == MODE_TOPKP) {
+  if ((R.mode == MODE_TOPK || R.mode == MODE_TOPKP) && bg_done && bnd) {
+    // the shard call wrote the local top-k over a -inf background; the global kept set is every
+    // candidate whose (key, ~global column) composite reaches the resolve's boundary: clear the rest
+    // (the rank's own sorted candidate list is in its send buffer: keys, then global columns)
+    const unsigned long long bd = bnd[r];
+    const int nl = kc_s[r];
+    const uint32_t *keys = send + B4 + (size_t)r * kmax;
+    const uint32_t *gid = send + B4 + (size_t)B * kmax + (size_t)r * kmax;
+    for (int i = tid; i < nl; i += kT) {
+      const uint32_t g = gid[i];
+      const unsigned long long cc = ((unsigned long long)keys[i] << 32) | (0xffffffffu - g);
+      if (cc >= bd) ++kept;
+      else o[(int64_t)g - offset] = ninf;
+    }
+  } else if (R.mode == MODE_TOPK || R.mode == MODE_TOPKP) {
     const int nw = (Vr + 31) >> 5;
     for (int i = tid; i < nw; i += kT) bm[i] = 0u;
     __syncthreads();
@@ -644,7 +660,8 @@ constexpr int kMergeT = 512;
 __global__ void __launch_bounds__(kMergeT) tp_merge_resolve(const uint32_t *recv, size_t send_words, int B4, int B,
                                                            int kmax, int world, int scap, int lp, int wp,
                                                            const int64_t *kk, const double *pp, TpRow *rows,
-                                                           int32_t *kidx_c, int32_t *kc_c, int W) {
+                                                           int32_t *kidx_c, int32_t *kc_c, int W,
+                                                           unsigned long long *bnd) {
   // lp: list slots (power of two >= kmax); wp: lists (power of two >= world); lp == 0: no merge tree
   extern __shared__ unsigned long long sk[];  // rank path: [W] lists | [scap] sorted | offsets
   unsigned long long *srt = world > 1 ? sk + W : sk;
@@ -783,7 +800,10 @@ __global__ void __launch_bounds__(kMergeT) tp_merge_resolve(const uint32_t *recv
   __syncthreads();
   const int L = (int)s_keep;
   for (int i = tid; i < L; i += kMergeT) kidx_c[(size_t)r * W + i] = (int32_t)(0xffffffffu - (uint32_t)srt[i]);
-  if (tid == 0) kc_c[r] = L;
+  if (tid == 0) {
+    kc_c[r] = L;
+    bnd[r] = L > 0 ? srt[L - 1] : ~0ull;  // the kept set is every candidate at or above this composite
+  }
 }
 
 // ------------------------------------------------------------------------------------------------
@@ -793,7 +813,7 @@ struct TpLayout {
   int kmax, W, B4;
   size_t send_words;
   size_t ws0, ws0_bytes, ws1, ws1_bytes, k_loc, p_one, k_c, p_c, kc_s, kidx_s, send, recv, cval, cgid, kidx_c,
-      kc_c, rows, tst, dl, part, part_loc, qbuf, total;
+      kc_c, bnd, rows, tst, dl, part, part_loc, qbuf, total;
 };
 
 inline TpLayout tp_layout(int B, int Vr, int world, int k_cap) {
@@ -826,6 +846,7 @@ inline TpLayout tp_layout(int B, int Vr, int world, int k_cap) {
   L.cgid = take(4ull * B * L.W);
   L.kidx_c = take(4ull * B * L.W);
   L.kc_c = take(4ull * B);
+  L.bnd = take(8ull * B);
   L.rows = take(sizeof(TpRow) * (size_t)B);
   L.tst = take(4ull * B);
   L.dl = take(8ull * 4 * B);
@@ -986,7 +1007,7 @@ int run_tp(const void *logits, int64_t ld_in, int dtype, int B, int Vr, int Vg, 
     merge_tree_shape(L, world, lp, wp);
     tp_merge_resolve<<<B, kMergeT, sb, st>>>((const uint32_t *)at(L.recv), L.send_words, L.B4, B, L.kmax, world,
                                              scap, lp, wp, k, p, rows, (int32_t *)at(L.kidx_c), (int32_t *)at(L.kc_c),
-                                             L.W);
+                                             L.W, (unsigned long long *)at(L.bnd));
     if (cudaGetLastError() != cudaSuccess) return QRITA_ECUDA;
   } else {
     tp_merge<<<B, kT, 0, st>>>((const uint32_t *)at(L.recv), L.send_words, L.B4, B, L.kmax, world, L.W, k, p, rows,
@@ -1017,12 +1038,14 @@ int run_tp(const void *logits, int64_t ld_in, int dtype, int B, int Vr, int Vg, 
   }
   // (4) the shard output
   const WsLayout W0 = ws_layout(B, Vr);
-  tp_write<T><<<B, kT, bm_bytes, st>>>(x, ld_in, (T *)out, ld_out, Vr, offset, rows,
+  tp_write<T><<<B, kT, (small && bg) ? 0 : bm_bytes, st>>>(x, ld_in, (T *)out, ld_out, Vr, offset, rows,
                                        small ? nullptr : (const uint32_t *)at(L.cgid),
                                        (const int32_t *)at(L.kidx_c), (const int32_t *)at(L.kc_c), L.W,
                                        (const uint32_t *)at(L.qbuf), rank, world, kept_count,
                                        (int32_t *)(ws + L.ws0 + W0.status), tst, sh, bg ? 1 : 0,
-                                       (const int32_t *)at(L.kidx_s), (const int32_t *)at(L.kc_s), L.kmax);
+                                       (const int32_t *)at(L.kidx_s), (const int32_t *)at(L.kc_s), L.kmax,
+                                       small ? (const unsigned long long *)at(L.bnd) : nullptr,
+                                       (const uint32_t *)at(L.send), L.B4, B);
   return cudaGetLastError() == cudaSuccess ? QRITA_OK : QRITA_ECUDA;
 }
 
