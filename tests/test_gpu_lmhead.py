@@ -38,13 +38,13 @@ def _kept_sets(idx, cnt):
 
 
 @pytest.mark.parametrize("b,v,d", [(4, 4096, 128), (37, 32000, 256), (130, 9000, 128), (300, 5000, 64),
-                                   (9, 1000, 64), (20, 2500, 128)])
+                                   (9, 1000, 64), (20, 2500, 128), (3, 100, 64), (17, 129, 64)])
 def test_fused_kept_sets_exact(cuda_device, b, v, d):
     h, w = _operands(b, v, d, 7 * b + v)
     if b > 5:
         h[5] = 0                                        # an all-tied row (every logit 0)
     rng = np.random.default_rng(b + v)
-    k = rng.integers(1, 1025, b).astype(np.int64)
+    k = np.minimum(rng.integers(1, 1025, b), v).astype(np.int64)
     p = rng.uniform(0.3, 0.99, b)
     k[::7] = v                                          # top-p only (whole row)
     p[1::5] = 1.0                                       # top-k only
