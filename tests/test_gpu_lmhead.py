@@ -108,3 +108,27 @@ def test_fused_compact_kept_lists(cuda_device):
     assert all(np.array_equal(a, c) for a, c in zip(_kept_sets(kidx, kc), want))
     with pytest.raises(ValueError):
         lm_head_topk_topp(h, w, k, p, k_cap=999)
+
+
+def test_capi_binding_as_documented(cuda_device):
+    """The INTEGRATION.md ctypes binding of qrita_lmhead_topk_topp, argument for argument."""
+    import ctypes
+    from paper_2602_01518_b200 import _native as N
+    lib = N.load()
+    B, V, d = 6, 3000, 128
+    hidden, weight = _operands(B, V, d, 21)
+    kt = torch.tensor([5, 50, 300, 1, 999, 64], dtype=torch.int64, device="cuda")
+    pt = torch.tensor([0.9, 0.5, 1.0, 1.0, 0.95, 0.8], dtype=torch.float64, device="cuda")
+    st = torch.cuda.current_stream().cuda_stream
+    nbytes = lib.qrita_lmhead_workspace_bytes(B, V)
+    ws = torch.zeros(nbytes + 256, dtype=torch.uint8, device="cuda"); wsp = (ws.data_ptr() + 255) & ~255
+    logits = torch.empty(B, V, device="cuda"); kidx = torch.empty(B, V, dtype=torch.int32, device="cuda")
+    kcnt = torch.empty(B, dtype=torch.int32, device="cuda")
+    rc = lib.qrita_lmhead_topk_topp(hidden.data_ptr(), d, weight.data_ptr(), d, B, V, d, kt.data_ptr(),
+                                    pt.data_ptr(), logits.data_ptr(), V, kidx.data_ptr(), V, kcnt.data_ptr(),
+                                    None, wsp, nbytes, 0, st)
+    assert rc == N.OK
+    row, col = ctypes.c_int(), ctypes.c_int()
+    assert lib.qrita_get_status(wsp, B, ctypes.byref(row), ctypes.byref(col), st) == N.OK
+    want = _kept_sets(*Q.topk_topp_indices(logits, kt, pt))
+    assert all(np.array_equal(a, c) for a, c in zip(_kept_sets(kidx, kcnt), want))
